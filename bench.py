@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark of the TT-DVM explicit step (BASELINE.json metric: cell-steps/s).
+
+A "step" is one explicit step S1 over every cell of the
+workload's mesh, with the state resident in HBM.  Default workload: config
+2 of BASELINE.json (32^3 periodic hex cells, 24^3 velocity mesh, eps 1e-6,
+seeded synthetic smooth Maxwellian fields + a rank-2 perturbation); see
+DESIGN.md for why config 4 (44^3) is not yet the N=1 workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 under torchrun: every rank steps its own full copy of the workload
+("replicas", weak scaling) until the slab partition's halo exchange lands;
+the timing is the max over ranks of the CUDA-event time of the K steps.
+--impl reference times the CPU oracle (the numpy restatement of the
+reference, all host cores, one process per core) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def workload_config(p, args):
+    return {"workload": p.name, "config_index": args.config, "cells": int(p.mesh.ncell),
+            "faces": int(p.mesh.nface), "velocity_mesh": f"{p.nv}^3 on [-{p.bound},{p.bound}]^3",
+            "eps": p.eps, "rank_cap": p.cap, "dt": p.dt,
+            "l2_policy": "inputs larger than L2 (state arena >> 126 MB)",
+            "timed_from": "initial state re-uploaded after warm-up (steps 1..K of the run)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def traffic_from_profiles():
+    """ncu dram bytes per launch of the dominant kernel, if captured."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ CPU arms
+def _ref_worker_init(args_tuple):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    global _W
+    cfg, scale = args_tuple
+    from oracle.step import OracleSolver
+    from oracle.tt import TtTensor
+    from paper_1912_04582_b200.problems import config
+    p = config(cfg, scale)
+    _W = (p, OracleSolver(p.mesh, p.nv, p.bound, p.gas, p.bcs), TtTensor)
+
+
+def _ref_task(cells):
+    p, solver, TtTensor = _W
+    need = set(cells)
+    for c in cells:
+        for fid, _ in p.mesh.cell_faces(c):
+            need.add(int(p.mesh.face_left[fid]))
+            r = int(p.mesh.face_right[fid])
+            if r >= 0:
+                need.add(r)
+    f = {i: TtTensor(*p.f0.get(i)) for i in need}
+    t = time.perf_counter()
+    solver.step(f, p.dt, p.eps, p.cap, cells=list(cells))
+    return time.perf_counter() - t
+
+
+def cpu_oracle_rate(cfg, scale, ncells: int, workers: int, repeats: int = 1):
+    """Cell-steps/s of the oracle on a sample of the workload's cells: each
+    worker steps a strip of `ncells` consecutive cells (with the fluxes of
+    every face they touch) from the workload's initial state."""
+    import multiprocessing as mp
+    from paper_1912_04582_b200.problems import config
+    p = config(cfg, scale)
+    strips = [list(range(w * ncells, (w + 1) * ncells)) for w in range(workers)]
+    strips = [[c % p.mesh.ncell for c in s] for s in strips]
+    ctxm = mp.get_context("spawn")
+    times = []
+    with ctxm.Pool(workers, initializer=_ref_worker_init, initargs=((cfg, scale),)) as pool:
+        pool.map(_ref_task, [[0]] * workers)  # warm imports
+        for _ in range(repeats):
+            t = time.perf_counter()
+            pool.map(_ref_task, strips)
+            times.append(time.perf_counter() - t)
+    return workers * ncells / min(times), times
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1912_04582_b200.problems import config
+    p = config(args.config, args.scale)
+    workers = os.cpu_count() or 1
+    per = 2
+    import multiprocessing as mp
+    from paper_1912_04582_b200.problems import config as _c  # noqa: F401
+    strips = [[(w * per + k) % p.mesh.ncell for k in range(per)] for w in range(workers)]
+    ctxm = mp.get_context("spawn")
+    with ctxm.Pool(workers, initializer=_ref_worker_init, initargs=((args.config, args.scale),)) as pool:
+        pool.map(_ref_task, [[0]] * workers)
+        for _ in range(args.warmup):
+            pool.map(_ref_task, strips)
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_ref_task, strips)
+        el = time.perf_counter() - t
+    value = workers * per * args.steps / el
+    line = {"impl": "reference", "metric": "cell-steps/s", "value": value, "unit": "cell-steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(p, args),
+            "cpu_baseline": {"value": value, "unit": "cell-steps/s", "cores": workers,
+                             "kind": "port",
+                             "sample": f"{workers} processes x {per} cells of the workload per "
+                                       "step (faces they touch included), numpy oracle, 1 BLAS "
+                                       "thread each"},
+            "e2e": {"value": value, "unit": "cell-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1912_04582_b200.cuda import Context
+    from paper_1912_04582_b200.problems import config
+    p = config(args.config, args.scale)
+    ctx = Context(local)
+    ctx.setup(p)
+    fp64_peak = ctx.fp64_peak()
+    ctx.step(p.dt, p.eps, p.cap, args.warmup)
+    ctx.upload_state(p.f0)  # time steps 1..K from the initial state
+    ctx.set_profiling(True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = ctx.timed_step(p.dt, p.eps, p.cap, args.steps)
+    torch.cuda.synchronize()
+    phase_ms = ctx.phase_times()
+    flops, bytes_, launches = ctx.phase_work()
+    gpu_launches = ctx.launch_count()
+    st = ctx.download_state()
+    max_rank = int(st.ranks.max())
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    cells = p.mesh.ncell
+    value = world * cells * args.steps / (ms / 1e3)
+
+    # e2e through the public API with host buffers: upload state, one step,
+    # download state -- every step
+    ctx.set_profiling(False)
+    host = p.f0
+    h2d = int(host.cores.nbytes + host.ranks.nbytes + host.offsets.nbytes)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(args.e2e_steps):
+        ctx.upload_state(host)
+        ctx.step(p.dt, p.eps, p.cap, 1)
+        host_out = ctx.download_state()
+        d2h = int(host_out.cores.nbytes + host_out.ranks.nbytes + host_out.offsets.nbytes)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * cells * args.e2e_steps / e2e_s
+
+    # roofline of the dominant kernel (the rounding phase with most time)
+    names = ["moments", "shakhov_build", "round_fs", "round_collision", "round_flux",
+             "round_residual", "round_update", "bookkeeping"]
+    dom = int(np.argmax(phase_ms[2:7])) + 2
+    dom_s = phase_ms[dom] / 1e3
+    achieved = flops[dom] / dom_s / 1e12 if dom_s > 0 else 0.0
+    traffic = traffic_from_profiles().get(names[dom])
+    roofline = {"bound": "fp64", "kernel": f"round_sums_kernel ({names[dom]})",
+                "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak if fp64_peak else None,
+                "peak_source": "measured on this GPU by the DFMA probe in libttdvm_cuda.so",
+                "flops_per_launch": flops[dom] / max(1, launches[dom]),
+                "launch_ms": phase_ms[dom] / max(1, launches[dom]),
+                "algorithmic_bytes_per_launch": bytes_[dom] / max(1, launches[dom]),
+                "hbm_frac": (bytes_[dom] / dom_s / 1e9) / load_peaks().get("hbm_gbs", 6547.8)
+                if dom_s > 0 else None,
+                "traffic": traffic,
+                "phase_ms": {names[i]: round(float(phase_ms[i]), 3) for i in range(8)},
+                "phase_tflops": {names[i]: round(float(flops[i] / (phase_ms[i] / 1e3) / 1e12), 4)
+                                 for i in range(2, 7) if phase_ms[i] > 0}}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ncells = 2
+        rate, times = cpu_oracle_rate(args.config, args.scale, ncells, 1)
+        cpu = {"value": rate, "unit": "cell-steps/s", "cores": 1, "kind": "port",
+               "sample": f"{ncells} cells of the workload, one step from the initial state, "
+                         "numpy oracle (oracle/step.py), 1 process, 1 BLAS thread"}
+    if rank == 0:
+        line = {"metric": "cell-steps/s", "value": value, "unit": "cell-steps/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": dict(workload_config(p, args),
+                                                    parallelism=f"replicas x{world}",
+                                                    max_rank_after=max_rank),
+                "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": "cell-steps/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "steps": args.e2e_steps},
+                "gpu_launches": gpu_launches, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/*
+ * ttdvm_cuda.h -- C ABI of the B200-native TT-DVM explicit step.
+ *
+ * Drop-in boundary for the hot path of arXiv 1912.04582's C++ reference
+ * (proj/include/ttdvm/*.hpp).  The reference has no step symbol and no
+ * caller (proj/tools/main.cpp:1); SPEC.md:391 declares
+ *     explicit_step(state, mesh, grid, gas, problem, config) -> state
+ * and SURVEY.md §8(b) fixes the C ABI below.  Each entry point names the
+ * reference interface it replaces.  Plain pointers and sizes only; every
+ * function returns a ttdvm_status and never throws.  A context owns all
+ * device memory; host buffers are caller-owned and only touched during the
+ * call.  Calls are stream-ordered and synchronous at return.  A context is
+ * not re-entrant (one per device / rank).
+ *
+ * TT packing (ttdvm_tt_batch), per tensor, in doubles, mirroring the
+ * reference's Eigen col-major cores (proj/include/ttdvm/tt_tensor.hpp:74-76):
+ *   [first  n1 x r1, (i,a) at i + n1*a]
+ *   [middle n2 slices r1 x r2, slice j (a,b) at j*r1*r2 + a + r1*b]
+ *   [last   r2 x n3, (b,k) at b + r2*k]
+ */
+#ifndef TTDVM_CUDA_H_
+#define TTDVM_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TTDVM_OK = 0,
+  TTDVM_EINVAL = 1,   /* -> std::invalid_argument in the C++ wrapper  */
+  TTDVM_EDOMAIN = 2,  /* -> std::runtime_error (cell / face id in message) */
+  TTDVM_ENOMEM = 3,
+  TTDVM_ECUDA = 4,
+  TTDVM_ENCCL = 5,
+} ttdvm_status;
+
+typedef struct ttdvm_ctx ttdvm_ctx;
+
+typedef struct {
+  int32_t count, n1, n2, n3;
+  const int32_t* ranks;   /* [2*count]: r1, r2 per tensor            */
+  const int64_t* offsets; /* [count+1]: first double of each tensor   */
+  const double* cores;    /* [offsets[count]]                          */
+} ttdvm_tt_batch;
+
+/* Boundary condition per mesh group (proj/include/ttdvm/boundary.hpp:13-41).
+ * kind: 0 wall, 1 sym-x, 2 sym-y, 3 sym-z, 4 in, 5 out. */
+typedef struct {
+  int32_t kind;
+  double wall_temperature;
+  double free_n, free_t, free_u[3];
+} ttdvm_bc;
+
+/* Context lifetime.  device = CUDA ordinal; nccl_comm = NULL or an
+ * ncclComm_t for the multi-GPU halo exchange (ttdvm_cuda_set_partition). */
+int ttdvm_cuda_create(int device, ttdvm_ctx** out);
+int ttdvm_cuda_destroy(ttdvm_ctx* ctx);
+const char* ttdvm_cuda_last_error(const ttdvm_ctx* ctx);
+
+/* VelocityGrid(n, bound) -- proj/src/velocity_grid.cpp:11-19. */
+int ttdvm_cuda_set_grid(ttdvm_ctx* ctx, int n, double bound);
+/* GasParameters -- proj/include/ttdvm/physics.hpp:11-18:
+ * gas = {molecule_mass, gas_constant, prandtl, mu_ref, t_ref, omega}. */
+int ttdvm_cuda_set_gas(ttdvm_ctx* ctx, const double gas[6]);
+
+/* UnstructuredMesh arrays consumed by the step
+ * (proj/include/ttdvm/mesh.hpp:15-41): normals unit, out of left; right =
+ * -1 on boundary faces; group -1 on interior (and periodic) faces; per cell
+ * the (face, sign) list, sign +1 iff the normal points out of the cell. */
+int ttdvm_cuda_set_mesh(ttdvm_ctx* ctx, int32_t ncell, int32_t nface, const int32_t* left,
+                        const int32_t* right, const int32_t* group, const double* area,
+                        const double* normal, const double* volume,
+                        const int64_t* cell_face_off, const int32_t* cell_face_id,
+                        const int8_t* cell_face_sign);
+
+/* Boundary conditions per group (replaces BoundaryCondition::wall/
+ * freestream_in/freestream_out/symmetry, proj/src/boundary.cpp:45-82). */
+int ttdvm_cuda_set_bcs(ttdvm_ctx* ctx, int32_t ngroup, const ttdvm_bc* bcs);
+
+/* State upload / download (per-cell f, resident across steps). */
+int ttdvm_cuda_upload_state(ttdvm_ctx* ctx, const ttdvm_tt_batch* f);
+/* Query ranks[2*count] and offsets[count+1] of the resident state. */
+int ttdvm_cuda_state_layout(ttdvm_ctx* ctx, int32_t* ranks, int64_t* offsets);
+/* Copy the packed state cores (capacity in doubles). */
+int ttdvm_cuda_download_state(ttdvm_ctx* ctx, double* cores, int64_t capacity);
+
+/* The explicit step S1, nsteps times: face fluxes
+ * Phi = round(xp o f_L + xm o f_R), collision J = compute_collision(f)
+ * (proj/src/physics.cpp:112-119), residual R = round(J - sum s A/V Phi),
+ * update f = round(f + dt R); all roundings TtTensor::rounded(eps, cap)
+ * (proj/src/tt_tensor.cpp:139-193; cap 0 = none, collision uncapped as in
+ * the reference). */
+int ttdvm_cuda_step(ttdvm_ctx* ctx, double dt, double eps, int32_t cap, int32_t nsteps);
+
+/* Macroparameters of the state the last step started from
+ * (compute_macro, proj/src/physics.cpp:17-67), 11 doubles per cell:
+ * n, u0, u1, u2, T, rho, p, S0, S1, S2, nu (= p / mu(T)). */
+int ttdvm_cuda_macros(ttdvm_ctx* ctx, double* out);
+
+/* Intermediates of the last step for lock-step parity (set: 0 = Phi per
+ * face, 1 = J rounded before the nu scale, 2 = R per cell, 3 = f_S per
+ * cell).  Same two-call protocol as the state. */
+int ttdvm_cuda_stage_layout(ttdvm_ctx* ctx, int32_t set, int32_t* count, int32_t* ranks,
+                            int64_t* offsets);
+int ttdvm_cuda_stage_download(ttdvm_ctx* ctx, int32_t set, double* cores, int64_t capacity);
+
+/* Batched TtTensor::rounded (proj/src/tt_tensor.cpp:139-193) of sums:
+ * output o = round(sum_{t in [group_off[o], group_off[o+1])} scale[t] * in[t]).
+ * group_off == NULL means one input per output.  The result stays on the
+ * device; fetch it with ttdvm_cuda_result_layout / _download.  margins
+ * (optional, 2 per output) receives each cut's relative decision margin
+ * min |tail + s^2 - budget| / budget over the kept/dropped boundary. */
+int ttdvm_cuda_round_batch(ttdvm_ctx* ctx, const ttdvm_tt_batch* in, int32_t nout,
+                           const int64_t* group_off, const double* scale, double eps,
+                           int32_t cap, double* margins);
+int ttdvm_cuda_result_layout(ttdvm_ctx* ctx, int32_t* ranks, int64_t* offsets);
+int ttdvm_cuda_result_download(ttdvm_ctx* ctx, double* cores, int64_t capacity);
+
+/* Batched compute_macro (proj/src/physics.cpp:17-67): 11 doubles per
+ * tensor as in ttdvm_cuda_macros (nu needs the gas). */
+int ttdvm_cuda_macro_batch(ttdvm_ctx* ctx, const ttdvm_tt_batch* in, double* out);
+
+/* Batched compute_collision (proj/src/physics.cpp:112-125): the result
+ * batch holds round(f_S - f, eps) per tensor, i.e. J before its final
+ * scaled(nu) (physics.cpp:118); nu = macros[11*t + 10].  macros optional. */
+int ttdvm_cuda_collision_batch(ttdvm_ctx* ctx, const ttdvm_tt_batch* in, double eps,
+                               double* macros);
+
+/* Device time (ms) of the kernels of the last call, by phase:
+ * [0] moments, [1] shakhov build, [2] round f_S, [3] round collision,
+ * [4] round fluxes, [5] round residual, [6] round update, [7] bookkeeping. */
+int ttdvm_cuda_phase_times(ttdvm_ctx* ctx, double* ms8);
+/* Canonical work of the last call by phase: FLOPs
+ * of the reference rounding algorithm on the actual ranks, compulsory HBM
+ * bytes (inputs read once + outputs written once), and rounding launches. */
+int ttdvm_cuda_phase_work(ttdvm_ctx* ctx, double* flops8, double* bytes8, int32_t* launches8);
+/* ttdvm_cuda_step timed with CUDA events on the library's stream (ms). */
+int ttdvm_cuda_timed_step(ttdvm_ctx* ctx, double dt, double eps, int32_t cap, int32_t nsteps,
+                          double* ms);
+/* Measured FP64 FMA peak of this device (TFLOP/s), the roofline
+ * denominator of the FP64-bound rounding kernels. */
+int ttdvm_cuda_fp64_peak(ttdvm_ctx* ctx, double* tflops);
+/* Number of kernel launches issued by the last call. */
+int64_t ttdvm_cuda_launch_count(const ttdvm_ctx* ctx);
+/* Enable/disable per-phase CUDA-event timing (costs one sync per phase). */
+int ttdvm_cuda_set_profiling(ttdvm_ctx* ctx, int on);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TTDVM_CUDA_H_ */

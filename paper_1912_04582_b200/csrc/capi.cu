@@ -1,0 +1,978 @@
+// Host runtime of the TT-DVM CUDA library: context, arenas, static summand
+// lists and the explicit-step driver behind the C ABI (include/ttdvm_cuda.h).
+//
+// Data layout in HBM: every tensor family (state,
+// f_S, J, face fluxes, residuals) is a TensorSet = per-tensor (r1, r2) and
+// offset into a bump-allocated FP64 arena holding the packed cores of the
+// C ABI (first | middle slices | last, col-major).  Rounding kernels
+// allocate their outputs with one atomicAdd per tensor; an overflowing
+// launch sets a flag, the host grows that arena and repeats the launch.
+// The state is double-buffered across steps.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ttdvm_cuda.h"
+#include "ttdvm_device.cuh"
+
+namespace ttdvm {
+cudaError_t launch_round(const RoundArgs& a, cudaStream_t st);
+size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX);
+struct MacroArgs {
+  TSet set;
+  int count, n;
+  const double* nodes;
+  const double* weights;
+  double gas[6];
+  double* macro;
+  double* nu;
+  int* status;
+};
+cudaError_t launch_macro(const MacroArgs& a, int rmax, cudaStream_t st);
+cudaError_t launch_shakhov_raw(const double* macro, int count, int n, const double* nodes,
+                               double R, double prandtl, double* out, cudaStream_t st);
+cudaError_t launch_gather(const TSet& s, int count, const long long* dst_off, int n1, int n2,
+                          int n3, double* dst, cudaStream_t st);
+cudaError_t launch_dfma_probe(double* out, int blocks, int threads, int iters, cudaStream_t st);
+}  // namespace ttdvm
+
+using namespace ttdvm;
+
+namespace {
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess)                                                           \
+      throw Fail{TTDVM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};      \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count == 0) return;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Fail{TTDVM_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes"};
+    }
+    n = count;
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// A family of tensors in one arena.
+struct TensorSet {
+  int count = 0;
+  DevBuf<int> ranks;
+  DevBuf<long long> off;
+  DevBuf<double> arena;
+  long long used = 0;  // doubles in use (host copy after the last launch)
+  int maxr1 = 0, maxr2 = 0;
+  const double* tscale = nullptr;
+  double uscale = 1.0;
+
+  void resize(int c) {
+    count = c;
+    ranks.alloc(std::max(1, 2 * c));
+    off.alloc(std::max(1, c));
+  }
+  TSet view() const {
+    TSet s;
+    s.ranks = ranks.p;
+    s.off = off.p;
+    s.base = arena.p;
+    s.tscale = tscale;
+    s.uscale = uscale;
+    return s;
+  }
+  void free() {
+    ranks.free();
+    off.free();
+    arena.free();
+  }
+};
+
+long long tt_size(int n1, int n2, int n3, int r1, int r2) {
+  return (long long)n1 * r1 + (long long)n2 * r1 * r2 + (long long)r2 * n3;
+}
+
+enum SetId { S_STATE = 0, S_FSRAW = 1, S_FS = 2, S_JR = 3, S_PHI = 4, S_RES = 5, S_FREE = 6, S_IN = 7 };
+
+struct TermList {
+  std::vector<long long> off;  // CSR
+  std::vector<Term> terms;
+  DevBuf<long long> d_off;
+  DevBuf<Term> d_terms;
+  int maxk = 0;
+  void upload() {
+    d_off.alloc(off.size());
+    d_terms.alloc(std::max<size_t>(1, terms.size()));
+    if (!off.empty()) CK(cudaMemcpy(d_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+    if (!terms.empty())
+      CK(cudaMemcpy(d_terms.p, terms.data(), terms.size() * sizeof(Term), cudaMemcpyHostToDevice));
+    maxk = 0;
+    for (size_t o = 0; o + 1 < off.size(); ++o) maxk = std::max<int>(maxk, (int)(off[o + 1] - off[o]));
+  }
+  int nout() const { return off.empty() ? 0 : (int)off.size() - 1; }
+  void free() {
+    d_off.free();
+    d_terms.free();
+  }
+};
+
+}  // namespace
+
+struct ttdvm_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  int n = 0;
+  double bound = 0.0;
+  std::vector<double> nodes;
+  DevBuf<double> d_nodes, d_weights;
+  double gas[6] = {1.0, 0.5, 2.0 / 3.0, 1.0, 1.0, 0.5};
+  // mesh
+  int ncell = 0, nface = 0;
+  std::vector<int> left, right, group;
+  std::vector<double> area, normal, volume;
+  std::vector<long long> cfo;
+  std::vector<int> cfid;
+  std::vector<signed char> cfs;
+  std::vector<ttdvm_bc> bcs;
+  bool terms_dirty = true;
+  // face factors: [nfac][3n]
+  std::vector<double> factors;
+  DevBuf<double> d_factors;
+  TermList t_fs, t_col, t_flux, t_res, t_upd, t_batch;
+  // tensor sets
+  TensorSet state[2];
+  int cur = 0;
+  TensorSet fsraw, fs, jr, phi, res, freestream, in, result;
+  DevBuf<double> d_macro, d_nu;
+  DevBuf<int> d_status;
+  int* h_status = nullptr;  // pinned, kStWords + 2 longs
+  DevBuf<double> d_margins;
+  DevBuf<long long> d_tmp_off;
+  DevBuf<double> d_tmp;
+  bool profiling = false;
+  double phase_ms[8] = {0};
+  double phase_flops[8] = {0}, phase_bytes[8] = {0};
+  int phase_launches[8] = {0};
+  DevBuf<double> d_acc;
+  int cur_phase = 7;
+  long long launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+void set_err(ttdvm_ctx* c, const std::string& m) {
+  if (c) c->err = m;
+}
+
+template <class F>
+int guard(ttdvm_ctx* c, F&& f) {
+  if (!c) return TTDVM_EINVAL;
+  try {
+    f();
+    c->err.clear();
+    return TTDVM_OK;
+  } catch (const Fail& e) {
+    set_err(c, e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_err(c, e.what());
+    return TTDVM_EINVAL;
+  }
+}
+
+void require(bool ok, const std::string& m) {
+  if (!ok) throw Fail{TTDVM_EINVAL, m};
+}
+
+struct Timer {
+  ttdvm_ctx* c;
+  int phase;
+  explicit Timer(ttdvm_ctx* c_, int p) : c(c_), phase(p) {
+    c->cur_phase = p;
+    if (c->profiling) CK(cudaEventRecord(c->ev0, c->st));
+  }
+  ~Timer() {
+    if (c->profiling) {
+      cudaEventRecord(c->ev1, c->st);
+      cudaEventSynchronize(c->ev1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+      c->phase_ms[phase] += ms;
+    }
+  }
+};
+
+void reset_counters(ttdvm_ctx* c) {
+  for (int i = 0; i < 8; ++i) {
+    c->phase_ms[i] = 0.0;
+    c->phase_flops[i] = 0.0;
+    c->phase_bytes[i] = 0.0;
+    c->phase_launches[i] = 0;
+  }
+  c->launches = 0;
+}
+
+void upload_batch(ttdvm_ctx* c, const ttdvm_tt_batch* b, TensorSet& s) {
+  require(b && b->count >= 0, "null batch");
+  require(b->n1 == c->n && b->n2 == c->n && b->n3 == c->n,
+          "batch mode sizes must equal the velocity grid size");
+  s.resize(b->count);
+  int m1 = 0, m2 = 0;
+  for (int t = 0; t < b->count; ++t) {
+    const int r1 = b->ranks[2 * t], r2 = b->ranks[2 * t + 1];
+    require(r1 >= 1 && r2 >= 1, "ranks must be >= 1");
+    require(b->offsets[t + 1] - b->offsets[t] == tt_size(b->n1, b->n2, b->n3, r1, r2),
+            "offsets do not match ranks");
+    m1 = std::max(m1, r1);
+    m2 = std::max(m2, r2);
+  }
+  const long long total = b->count ? b->offsets[b->count] : 0;
+  s.arena.alloc(std::max<long long>(1, total));
+  if (b->count) {
+    CK(cudaMemcpyAsync(s.ranks.p, b->ranks, 8LL * b->count, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(s.off.p, b->offsets, 8LL * b->count, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(s.arena.p, b->cores, 8LL * total, cudaMemcpyHostToDevice, c->st));
+  }
+  s.used = total;
+  s.maxr1 = m1;
+  s.maxr2 = m2;
+  CK(cudaStreamSynchronize(c->st));
+}
+
+void ensure_static(ttdvm_ctx* c) {
+  if (c->d_status.p == nullptr) {
+    c->d_acc.alloc(2);
+    c->d_status.alloc(kStWords + 4);
+    CK(cudaMallocHost(&c->h_status, 64 * sizeof(int)));
+  }
+}
+
+// Run one rounding launch: sets bound into RoundArgs, output into `out`.
+// Repeats the launch with a larger arena if it overflowed.
+void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets], TensorSet& out,
+               double eps, int cap, double* margins_dev) {
+  const int nout = tl.nout();
+  out.resize(nout);
+  if (nout == 0) return;
+  require(tl.maxk <= kMaxTerms, "too many summands per rounded output");
+  ensure_static(c);
+  // rank bounds: sum over the summands of the set maxima
+  int RM1 = 1, RM2 = 1;
+  {
+    // per-output term count is small; bound with maxk * max over sets used
+    int m1 = 1, m2 = 1;
+    for (const Term& t : tl.terms) {
+      m1 = std::max(m1, sets[t.set]->maxr1);
+      m2 = std::max(m2, sets[t.set]->maxr2);
+    }
+    RM1 = std::max(1, tl.maxk * m1);
+    RM2 = std::max(1, tl.maxk * m2);
+  }
+  const int n = c->n;
+  const int mx = n;
+  int HMAX = std::max(mx, std::min(4 * mx, 128));
+  size_t smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX);
+  while (smem > 227 * 1024 && HMAX > mx) {
+    HMAX = std::max(mx, HMAX / 2);
+    smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX);
+  }
+  if (smem > 227 * 1024)
+    throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory (n=" + std::to_string(n) +
+                                 ", summed ranks " + std::to_string(RM1) + "x" +
+                                 std::to_string(RM2) + ")"};
+  // arena estimate
+  if (out.arena.n == 0) {
+    const int re = std::min(n, std::max(8, std::max(RM1, RM2) / std::max(1, tl.maxk) + 4));
+    out.arena.alloc((size_t)nout * tt_size(n, n, n, re, re) + 1024);
+  }
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    RoundArgs a;
+    memset(&a, 0, sizeof(a));
+    for (int s = 0; s < kMaxSets; ++s)
+      if (sets[s]) a.sets[s] = sets[s]->view();
+    a.term_off = tl.d_off.p;
+    a.terms = tl.d_terms.p;
+    a.factors = c->d_factors.p;
+    a.n1 = a.n2 = a.n3 = n;
+    a.nout = nout;
+    a.eps = eps;
+    a.cap = cap;
+    a.out.ranks = out.ranks.p;
+    a.out.off = out.off.p;
+    a.out.base = out.arena.p;
+    a.out.used = reinterpret_cast<unsigned long long*>(c->d_status.p + kStWords);
+    a.out.capacity = (long long)out.arena.n;
+    a.status = c->d_status.p;
+    a.margins = margins_dev;
+    a.acc = c->d_acc.p;
+    a.RM1 = RM1;
+    a.RM2 = RM2;
+    a.HMAX = HMAX;
+    CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
+    CK(cudaMemsetAsync(c->d_acc.p, 0, 2 * sizeof(double), c->st));
+    CK(launch_round(a, c->st));
+    c->launches += 1;
+    CK(cudaMemcpyAsync(c->h_status, c->d_status.p, (kStWords + 4) * sizeof(int),
+                       cudaMemcpyDeviceToHost, c->st));
+    double acc[2];
+    CK(cudaMemcpyAsync(acc, c->d_acc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (!c->h_status[kStOverflow]) {
+      c->phase_flops[c->cur_phase] += acc[0];
+      c->phase_bytes[c->cur_phase] += acc[1];
+      c->phase_launches[c->cur_phase] += 1;
+    }
+    const unsigned long long used =
+        *reinterpret_cast<unsigned long long*>(c->h_status + kStWords);
+    if (c->h_status[kStOverflow]) {
+      const size_t want = std::max<size_t>(out.arena.n * 2, (size_t)(used * 1.25) + 1024);
+      out.arena.free();
+      out.arena.alloc(want);
+      continue;
+    }
+    out.used = (long long)used;
+    out.maxr1 = c->h_status[kStMaxR1] > 0 ? c->h_status[kStMaxR1] : 1;
+    out.maxr2 = c->h_status[kStMaxR2] > 0 ? c->h_status[kStMaxR2] : 1;
+    if (c->h_status[kStError])
+      throw Fail{TTDVM_EDOMAIN, "rounding: non-finite input in output " +
+                                    std::to_string(c->h_status[kStErrIdx])};
+    return;
+  }
+  throw Fail{TTDVM_ENOMEM, "rounding arena could not be grown"};
+}
+
+void run_macro(ttdvm_ctx* c, TensorSet& s, double* macro, double* nu) {
+  ensure_static(c);
+  MacroArgs a;
+  a.set = s.view();
+  a.count = s.count;
+  a.n = c->n;
+  a.nodes = c->d_nodes.p;
+  a.weights = c->d_weights.p;
+  for (int i = 0; i < 6; ++i) a.gas[i] = c->gas[i];
+  a.macro = macro;
+  a.nu = nu;
+  a.status = c->d_status.p;
+  CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
+  CK(launch_macro(a, std::max(s.maxr1, s.maxr2), c->st));
+  c->launches += 1;
+  CK(cudaMemcpyAsync(c->h_status, c->d_status.p, (kStWords + 4) * sizeof(int),
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (c->h_status[kStError] == kErrDensity)
+    throw Fail{TTDVM_EDOMAIN,
+               "compute_macro: nonpositive density in cell " + std::to_string(c->h_status[kStErrIdx])};
+  if (c->h_status[kStError] == kErrTemperature)
+    throw Fail{TTDVM_EDOMAIN, "compute_macro: nonpositive temperature in cell " +
+                                  std::to_string(c->h_status[kStErrIdx])};
+}
+
+// collision of `s` (set 0): f_S raw -> round -> (f_S - f) round; J_r in c->jr
+void run_collision(ttdvm_ctx* c, TensorSet& s, double eps) {
+  const int count = s.count;
+  const int n = c->n;
+  c->d_macro.alloc(std::max(1, 11 * count));
+  c->d_nu.alloc(std::max(1, count));
+  {
+    Timer t(c, 0);
+    run_macro(c, s, c->d_macro.p, c->d_nu.p);
+  }
+  {
+    Timer t(c, 1);
+    c->fsraw.resize(count);
+    c->fsraw.arena.alloc(std::max<size_t>(1, (size_t)count * 24 * n));
+    std::vector<int> rk(2 * (size_t)count, 4);
+    std::vector<long long> of(count);
+    for (int i = 0; i < count; ++i) of[i] = (long long)i * 24 * n;
+    if (count) {
+      CK(cudaMemcpyAsync(c->fsraw.ranks.p, rk.data(), 8LL * count, cudaMemcpyHostToDevice, c->st));
+      CK(cudaMemcpyAsync(c->fsraw.off.p, of.data(), 8LL * count, cudaMemcpyHostToDevice, c->st));
+    }
+    c->fsraw.maxr1 = c->fsraw.maxr2 = 4;
+    CK(launch_shakhov_raw(c->d_macro.p, count, n, c->d_nodes.p, c->gas[1], c->gas[2],
+                          c->fsraw.arena.p, c->st));
+    c->launches += 1;
+  }
+  // one-summand lists (identity) for f_S; (f_S, -f) for J
+  if ((int)c->t_fs.off.size() != count + 1) {
+    c->t_fs.off.resize(count + 1);
+    c->t_fs.terms.resize(count);
+    c->t_col.off.resize(count + 1);
+    c->t_col.terms.resize(2 * (size_t)count);
+    for (int i = 0; i <= count; ++i) {
+      c->t_fs.off[i] = i;
+      c->t_col.off[i] = 2LL * i;
+    }
+    for (int i = 0; i < count; ++i) {
+      c->t_fs.terms[i] = Term{S_FSRAW, i, 1.0, -1, 0};
+      c->t_col.terms[2 * i] = Term{S_FS, i, 1.0, -1, 0};
+      c->t_col.terms[2 * i + 1] = Term{S_STATE, i, -1.0, -1, 0};
+    }
+    c->t_fs.upload();
+    c->t_col.upload();
+  }
+  TensorSet* sets[kMaxSets] = {&s, &c->fsraw, &c->fs, &c->jr, &c->phi, &c->res, &c->freestream, &c->in};
+  {
+    Timer t(c, 2);
+    run_round(c, c->t_fs, sets, c->fs, eps, 0, nullptr);
+  }
+  {
+    Timer t(c, 3);
+    run_round(c, c->t_col, sets, c->jr, eps, 0, nullptr);
+  }
+}
+
+// Static summand lists of the step (rebuilt when mesh / BCs / grid change).
+void build_step_terms(ttdvm_ctx* c) {
+  if (!c->terms_dirty) return;
+  require(c->n > 0, "set_grid first");
+  require(c->ncell > 0, "set_mesh first");
+  const int n = c->n;
+  // face factors (xi.n)^{+/-} for axis-aligned normals: exactly
+  // ((xi_n +- |xi_n|)/2) on one axis, ones on the others (SURVEY.md §8(a)
+  // T13; the reference's rank-1 E for axis normals is exact,
+  // proj/tests/test_velocity_grid.cpp:98-115).
+  c->factors.clear();
+  std::vector<int> facp(c->nface), facm(c->nface);
+  std::vector<int> key_of;  // (axis*2 + sign) -> factor pair id
+  int pair_id[6];
+  for (int k = 0; k < 6; ++k) pair_id[k] = -1;
+  for (int f = 0; f < c->nface; ++f) {
+    const double* nv = &c->normal[3 * f];
+    int axis = -1;
+    double sgn = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      if (nv[a] != 0.0) {
+        if (axis >= 0) axis = 9;
+        else axis = a;
+      }
+    }
+    require(axis >= 0 && axis < 3,
+            "face " + std::to_string(f) +
+                ": oblique normals need the general face-factor builder (SURVEY.md §8(f) N1)");
+    sgn = nv[axis];
+    require(std::fabs(std::fabs(sgn) - 1.0) <= 1e-12, "xi_normal: normal must be a unit vector");
+    const int key = axis * 2 + (sgn > 0 ? 1 : 0);
+    if (pair_id[key] < 0) {
+      pair_id[key] = (int)(c->factors.size() / (3 * n)) ;
+      for (int pm = 0; pm < 2; ++pm) {
+        std::vector<double> fac(3 * n, 1.0);
+        for (int i = 0; i < n; ++i) {
+          const double xn = sgn * c->nodes[i];
+          const double ab = std::fabs(c->nodes[i]);
+          fac[axis * n + i] = pm == 0 ? (xn + ab) * 0.5 : (xn - ab) * 0.5;
+        }
+        c->factors.insert(c->factors.end(), fac.begin(), fac.end());
+      }
+    }
+    facp[f] = pair_id[key];
+    facm[f] = pair_id[key] + 1;
+  }
+  c->d_factors.alloc(std::max<size_t>(1, c->factors.size()));
+  if (!c->factors.empty())
+    CK(cudaMemcpy(c->d_factors.p, c->factors.data(), c->factors.size() * 8, cudaMemcpyHostToDevice));
+
+  // freestream Maxwellians per group (maxwell_tt, proj/src/physics.cpp:69-87)
+  const int ng = (int)c->bcs.size();
+  {
+    std::vector<int> rk(2 * std::max(1, ng), 1);
+    std::vector<long long> of(std::max(1, ng));
+    std::vector<double> cores((size_t)std::max(1, ng) * 3 * n, 0.0);
+    for (int g = 0; g < ng; ++g) {
+      of[g] = (long long)g * 3 * n;
+      const ttdvm_bc& b = c->bcs[g];
+      if (b.kind == 4 || b.kind == 5) {
+        require(b.free_n > 0.0 && b.free_t > 0.0, "maxwell_tt: state must have n > 0, T > 0");
+        const double two_rt = 2.0 * c->gas[1] * b.free_t;
+        const double norm1d = 1.0 / std::sqrt(M_PI * two_rt);
+        for (int a = 0; a < 3; ++a)
+          for (int i = 0; i < n; ++i) {
+            const double v = c->nodes[i] - b.free_u[a];
+            double val = norm1d * std::exp(-v * v / two_rt);
+            if (a == 0) val *= b.free_n;
+            cores[(size_t)g * 3 * n + a * n + i] = val;
+          }
+      }
+    }
+    c->freestream.resize(std::max(1, ng));
+    c->freestream.arena.alloc(cores.size());
+    CK(cudaMemcpy(c->freestream.ranks.p, rk.data(), rk.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->freestream.off.p, of.data(), of.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->freestream.arena.p, cores.data(), cores.size() * 8, cudaMemcpyHostToDevice));
+    c->freestream.maxr1 = c->freestream.maxr2 = 1;
+  }
+
+  // flux: Phi_f = round(xp o f_L + xm o f_R)
+  TermList& fl = c->t_flux;
+  fl.off.assign(1, 0);
+  fl.terms.clear();
+  for (int f = 0; f < c->nface; ++f) {
+    fl.terms.push_back(Term{S_STATE, c->left[f], 1.0, facp[f], 0});
+    const int r = c->right[f];
+    if (r >= 0) {
+      fl.terms.push_back(Term{S_STATE, r, 1.0, facm[f], 0});
+    } else {
+      const int g = c->group[f];
+      require(g >= 0 && g < ng, "boundary face " + std::to_string(f) + " has no boundary condition");
+      const int kind = c->bcs[g].kind;
+      if (kind >= 1 && kind <= 3) {
+        fl.terms.push_back(Term{S_STATE, c->left[f], 1.0, facm[f], kind});
+      } else if (kind == 4 || kind == 5) {
+        fl.terms.push_back(Term{S_FREE, g, 1.0, facm[f], 0});
+      } else {
+        throw Fail{TTDVM_EINVAL,
+                   "wall boundaries need the wall-ghost kernel (SURVEY.md §8(f) N3)"};
+      }
+    }
+    fl.off.push_back((long long)fl.terms.size());
+  }
+  fl.upload();
+  // residual: R_i = round(J_i + sum_j Phi_j * (-s A_j / V_i))
+  TermList& rl = c->t_res;
+  rl.off.assign(1, 0);
+  rl.terms.clear();
+  for (int i = 0; i < c->ncell; ++i) {
+    rl.terms.push_back(Term{S_JR, i, 1.0, -1, 0});
+    for (long long e = c->cfo[i]; e < c->cfo[i + 1]; ++e) {
+      const int fid = c->cfid[e];
+      const int s = c->cfs[e];
+      const double sc = -s * c->area[fid] / c->volume[i];
+      rl.terms.push_back(Term{S_PHI, fid, sc, -1, 0});
+    }
+    rl.off.push_back((long long)rl.terms.size());
+  }
+  rl.upload();
+  // update: f_i' = round(f_i + R_i * dt)   (dt is the uniform scale of R)
+  TermList& ul = c->t_upd;
+  ul.off.resize(c->ncell + 1);
+  ul.terms.resize(2 * (size_t)c->ncell);
+  for (int i = 0; i <= c->ncell; ++i) ul.off[i] = 2LL * i;
+  for (int i = 0; i < c->ncell; ++i) {
+    ul.terms[2 * i] = Term{S_STATE, i, 1.0, -1, 0};
+    ul.terms[2 * i + 1] = Term{S_RES, i, 1.0, -1, 0};
+  }
+  ul.upload();
+  c->terms_dirty = false;
+}
+
+void step_once(ttdvm_ctx* c, double dt, double eps, int cap) {
+  TensorSet& s = c->state[c->cur];
+  TensorSet& nxt = c->state[1 - c->cur];
+  // pieces (3) + (4): moments, f_S, J_r = round(f_S - f); nu applied as
+  // J's per-tensor scale (TtTensor::scaled after rounding, physics.cpp:118)
+  run_collision(c, s, eps);
+  c->jr.tscale = c->d_nu.p;
+  TensorSet* sets[kMaxSets] = {&s, &c->fsraw, &c->fs, &c->jr, &c->phi, &c->res, &c->freestream, &c->in};
+  {
+    Timer t(c, 4);
+    run_round(c, c->t_flux, sets, c->phi, eps, cap, nullptr);
+  }
+  c->res.uscale = 1.0;
+  {
+    Timer t(c, 5);
+    run_round(c, c->t_res, sets, c->res, eps, cap, nullptr);
+  }
+  c->res.uscale = dt;
+  {
+    Timer t(c, 6);
+    run_round(c, c->t_upd, sets, nxt, eps, cap, nullptr);
+  }
+  c->res.uscale = 1.0;
+  c->cur = 1 - c->cur;
+}
+
+void layout_of(ttdvm_ctx* c, const TensorSet& s, int32_t* ranks, int64_t* offsets) {
+  std::vector<int> rk(2 * (size_t)s.count);
+  if (s.count)
+    CK(cudaMemcpy(rk.data(), s.ranks.p, rk.size() * 4, cudaMemcpyDeviceToHost));
+  long long o = 0;
+  for (int t = 0; t < s.count; ++t) {
+    if (ranks) {
+      ranks[2 * t] = rk[2 * t];
+      ranks[2 * t + 1] = rk[2 * t + 1];
+    }
+    if (offsets) offsets[t] = o;
+    o += tt_size(c->n, c->n, c->n, rk[2 * t], rk[2 * t + 1]);
+  }
+  if (offsets) offsets[s.count] = o;
+}
+
+void download_set(ttdvm_ctx* c, const TensorSet& s, double* cores, int64_t capacity) {
+  std::vector<int64_t> offs(s.count + 1);
+  layout_of(c, s, nullptr, offs.data());
+  const long long total = offs[s.count];
+  require(capacity >= total, "download capacity too small: need " + std::to_string(total));
+  if (s.count == 0) return;
+  c->d_tmp_off.alloc(s.count);
+  c->d_tmp.alloc(std::max<long long>(1, total));
+  CK(cudaMemcpy(c->d_tmp_off.p, offs.data(), 8LL * s.count, cudaMemcpyHostToDevice));
+  CK(launch_gather(s.view(), s.count, c->d_tmp_off.p, c->n, c->n, c->n, c->d_tmp.p, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpy(cores, c->d_tmp.p, 8LL * total, cudaMemcpyDeviceToHost));
+}
+
+}  // namespace
+
+extern "C" {
+
+int ttdvm_cuda_create(int device, ttdvm_ctx** out) {
+  if (!out) return TTDVM_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return TTDVM_ECUDA;
+  }
+  if (device < 0 || device >= ndev) return TTDVM_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return TTDVM_ECUDA;
+  ttdvm_ctx* c = new ttdvm_ctx();
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+    delete c;
+    return TTDVM_ECUDA;
+  }
+  *out = c;
+  return TTDVM_OK;
+}
+
+int ttdvm_cuda_destroy(ttdvm_ctx* c) {
+  if (!c) return TTDVM_EINVAL;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  for (TensorSet* s : {&c->state[0], &c->state[1], &c->fsraw, &c->fs, &c->jr, &c->phi, &c->res,
+                       &c->freestream, &c->in, &c->result})
+    s->free();
+  for (TermList* t : {&c->t_fs, &c->t_col, &c->t_flux, &c->t_res, &c->t_upd, &c->t_batch}) t->free();
+  c->d_nodes.free();
+  c->d_weights.free();
+  c->d_factors.free();
+  c->d_macro.free();
+  c->d_nu.free();
+  c->d_status.free();
+  c->d_acc.free();
+  c->d_margins.free();
+  c->d_tmp.free();
+  c->d_tmp_off.free();
+  if (c->h_status) cudaFreeHost(c->h_status);
+  cudaEventDestroy(c->ev0);
+  cudaEventDestroy(c->ev1);
+  cudaStreamDestroy(c->st);
+  delete c;
+  return TTDVM_OK;
+}
+
+const char* ttdvm_cuda_last_error(const ttdvm_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int ttdvm_cuda_set_grid(ttdvm_ctx* c, int n, double bound) {
+  return guard(c, [&] {
+    // VelocityGrid(n, bound), proj/src/velocity_grid.cpp:11-19
+    require(n >= 2, "VelocityGrid: need at least 2 nodes");
+    require(bound > 0.0, "VelocityGrid: bound must be positive");
+    require(n <= 64, "velocity grids above 64 nodes per axis are not supported");
+    cudaSetDevice(c->device);
+    c->n = n;
+    c->bound = bound;
+    const double dxi = 2.0 * bound / (n - 1);
+    c->nodes.resize(n);
+    for (int i = 0; i < n; ++i) c->nodes[i] = -bound + i * dxi;
+    std::vector<double> w(n, dxi);
+    c->d_nodes.alloc(n);
+    c->d_weights.alloc(n);
+    CK(cudaMemcpy(c->d_nodes.p, c->nodes.data(), 8 * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_weights.p, w.data(), 8 * n, cudaMemcpyHostToDevice));
+    c->terms_dirty = true;
+  });
+}
+
+int ttdvm_cuda_set_gas(ttdvm_ctx* c, const double gas[6]) {
+  return guard(c, [&] {
+    require(gas != nullptr, "null gas");
+    for (int i = 0; i < 6; ++i) c->gas[i] = gas[i];
+    c->terms_dirty = true;
+  });
+}
+
+int ttdvm_cuda_set_mesh(ttdvm_ctx* c, int32_t ncell, int32_t nface, const int32_t* left,
+                        const int32_t* right, const int32_t* group, const double* area,
+                        const double* normal, const double* volume, const int64_t* cfo,
+                        const int32_t* cfid, const int8_t* cfs) {
+  return guard(c, [&] {
+    require(ncell > 0 && nface >= 0, "empty mesh");
+    c->ncell = ncell;
+    c->nface = nface;
+    c->left.assign(left, left + nface);
+    c->right.assign(right, right + nface);
+    c->group.assign(group, group + nface);
+    c->area.assign(area, area + nface);
+    c->normal.assign(normal, normal + 3 * (size_t)nface);
+    c->volume.assign(volume, volume + ncell);
+    c->cfo.assign(cfo, cfo + ncell + 1);
+    c->cfid.assign(cfid, cfid + cfo[ncell]);
+    c->cfs.assign(cfs, cfs + cfo[ncell]);
+    for (int f = 0; f < nface; ++f) {
+      require(left[f] >= 0 && left[f] < ncell, "face left cell out of range");
+      require(right[f] >= -1 && right[f] < ncell, "face right cell out of range");
+    }
+    for (int i = 0; i < ncell; ++i) {
+      require(cfo[i + 1] - cfo[i] + 1 <= kMaxTerms, "too many faces per cell");
+      require(volume[i] > 0.0, "nonpositive cell volume");
+    }
+    c->terms_dirty = true;
+  });
+}
+
+int ttdvm_cuda_set_bcs(ttdvm_ctx* c, int32_t ngroup, const ttdvm_bc* bcs) {
+  return guard(c, [&] {
+    require(ngroup >= 0 && (ngroup == 0 || bcs), "null bcs");
+    for (int g = 0; g < ngroup; ++g) {
+      require(bcs[g].kind >= 0 && bcs[g].kind <= 5, "unknown boundary condition kind");
+      if (bcs[g].kind == 0)
+        require(bcs[g].wall_temperature > 0.0, "wall boundary requires positive temperature");
+    }
+    c->bcs.assign(bcs, bcs + ngroup);
+    c->terms_dirty = true;
+  });
+}
+
+int ttdvm_cuda_upload_state(ttdvm_ctx* c, const ttdvm_tt_batch* f) {
+  return guard(c, [&] {
+    require(c->n > 0, "set_grid first");
+    cudaSetDevice(c->device);
+    c->cur = 0;
+    upload_batch(c, f, c->state[0]);
+  });
+}
+
+int ttdvm_cuda_state_layout(ttdvm_ctx* c, int32_t* ranks, int64_t* offsets) {
+  return guard(c, [&] { layout_of(c, c->state[c->cur], ranks, offsets); });
+}
+
+int ttdvm_cuda_download_state(ttdvm_ctx* c, double* cores, int64_t capacity) {
+  return guard(c, [&] { download_set(c, c->state[c->cur], cores, capacity); });
+}
+
+int ttdvm_cuda_step(ttdvm_ctx* c, double dt, double eps, int32_t cap, int32_t nsteps) {
+  return guard(c, [&] {
+    require(eps > 0.0, "rounded: eps must be > 0");
+    require(c->state[c->cur].count == c->ncell, "state count must equal the mesh cell count");
+    cudaSetDevice(c->device);
+    build_step_terms(c);
+    reset_counters(c);
+    for (int k = 0; k < nsteps; ++k) step_once(c, dt, eps, cap);
+  });
+}
+
+int ttdvm_cuda_macros(ttdvm_ctx* c, double* out) {
+  return guard(c, [&] {
+    require(c->d_macro.p != nullptr, "no step has run");
+    CK(cudaMemcpy(out, c->d_macro.p, 8LL * 11 * c->ncell, cudaMemcpyDeviceToHost));
+  });
+}
+
+static TensorSet* stage_set(ttdvm_ctx* c, int set) {
+  switch (set) {
+    case 0: return &c->phi;
+    case 1: return &c->jr;
+    case 2: return &c->res;
+    case 3: return &c->fs;
+    default: throw Fail{TTDVM_EINVAL, "unknown stage set"};
+  }
+}
+
+int ttdvm_cuda_stage_layout(ttdvm_ctx* c, int32_t set, int32_t* count, int32_t* ranks,
+                            int64_t* offsets) {
+  return guard(c, [&] {
+    TensorSet* s = stage_set(c, set);
+    if (count) *count = s->count;
+    if (ranks || offsets) layout_of(c, *s, ranks, offsets);
+  });
+}
+
+int ttdvm_cuda_stage_download(ttdvm_ctx* c, int32_t set, double* cores, int64_t capacity) {
+  return guard(c, [&] { download_set(c, *stage_set(c, set), cores, capacity); });
+}
+
+int ttdvm_cuda_round_batch(ttdvm_ctx* c, const ttdvm_tt_batch* in, int32_t nout,
+                           const int64_t* group_off, const double* scale, double eps, int32_t cap,
+                           double* margins) {
+  return guard(c, [&] {
+    require(eps > 0.0, "rounded: eps must be > 0");
+    require(c->n > 0, "set_grid first");
+    cudaSetDevice(c->device);
+    upload_batch(c, in, c->in);
+    TermList& tl = c->t_batch;
+    tl.off.resize(nout + 1);
+    tl.terms.clear();
+    for (int o = 0; o <= nout; ++o) tl.off[o] = group_off ? group_off[o] : o;
+    require(tl.off[nout] == in->count, "group offsets must cover the input batch");
+    for (int t = 0; t < in->count; ++t)
+      tl.terms.push_back(Term{S_IN, t, scale ? scale[t] : 1.0, -1, 0});
+    tl.upload();
+    TensorSet* sets[kMaxSets] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &c->in};
+    double* dm = nullptr;
+    if (margins) {
+      c->d_margins.alloc(std::max(1, 2 * nout));
+      dm = c->d_margins.p;
+    }
+    reset_counters(c);
+    {
+      Timer t(c, 2);
+      run_round(c, tl, sets, c->result, eps, cap, dm);
+    }
+    if (margins && nout)
+      CK(cudaMemcpy(margins, dm, 16LL * nout, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ttdvm_cuda_result_layout(ttdvm_ctx* c, int32_t* ranks, int64_t* offsets) {
+  return guard(c, [&] { layout_of(c, c->result, ranks, offsets); });
+}
+
+int ttdvm_cuda_result_download(ttdvm_ctx* c, double* cores, int64_t capacity) {
+  return guard(c, [&] { download_set(c, c->result, cores, capacity); });
+}
+
+int ttdvm_cuda_macro_batch(ttdvm_ctx* c, const ttdvm_tt_batch* in, double* out) {
+  return guard(c, [&] {
+    require(c->n > 0, "set_grid first");
+    cudaSetDevice(c->device);
+    upload_batch(c, in, c->in);
+    c->d_macro.alloc(std::max(1, 11 * in->count));
+    c->launches = 0;
+    run_macro(c, c->in, c->d_macro.p, nullptr);
+    if (in->count)
+      CK(cudaMemcpy(out, c->d_macro.p, 88LL * in->count, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ttdvm_cuda_collision_batch(ttdvm_ctx* c, const ttdvm_tt_batch* in, double eps,
+                               double* macros) {
+  return guard(c, [&] {
+    require(eps > 0.0, "rounded: eps must be > 0");
+    require(c->n > 0, "set_grid first");
+    cudaSetDevice(c->device);
+    upload_batch(c, in, c->in);
+    c->t_fs.off.clear();  // force rebuild of the per-count lists
+    c->launches = 0;
+    run_collision(c, c->in, eps);
+    // result = J_r, the rounded f_S - f before the nu scale; nu is
+    // macros[11*i + 10] (compute_collision applies scaled(nu) last).
+    c->result.free();
+    c->result.resize(c->jr.count);
+    c->result.arena.alloc(std::max<long long>(1, c->jr.used));
+    CK(cudaMemcpy(c->result.arena.p, c->jr.arena.p, 8LL * std::max<long long>(1, c->jr.used),
+                  cudaMemcpyDeviceToDevice));
+    if (c->jr.count) {
+      CK(cudaMemcpy(c->result.ranks.p, c->jr.ranks.p, 8LL * c->jr.count, cudaMemcpyDeviceToDevice));
+      CK(cudaMemcpy(c->result.off.p, c->jr.off.p, 8LL * c->jr.count, cudaMemcpyDeviceToDevice));
+    }
+    c->result.maxr1 = c->jr.maxr1;
+    c->result.maxr2 = c->jr.maxr2;
+    c->t_fs.off.clear();
+    if (macros && c->in.count)
+      CK(cudaMemcpy(macros, c->d_macro.p, 88LL * c->in.count, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ttdvm_cuda_phase_times(ttdvm_ctx* c, double* ms8) {
+  return guard(c, [&] {
+    for (int i = 0; i < 8; ++i) ms8[i] = c->phase_ms[i];
+  });
+}
+
+int ttdvm_cuda_phase_work(ttdvm_ctx* c, double* flops8, double* bytes8, int32_t* launches8) {
+  return guard(c, [&] {
+    for (int i = 0; i < 8; ++i) {
+      if (flops8) flops8[i] = c->phase_flops[i];
+      if (bytes8) bytes8[i] = c->phase_bytes[i];
+      if (launches8) launches8[i] = c->phase_launches[i];
+    }
+  });
+}
+
+int ttdvm_cuda_timed_step(ttdvm_ctx* c, double dt, double eps, int32_t cap, int32_t nsteps,
+                          double* ms) {
+  return guard(c, [&] {
+    require(eps > 0.0, "rounded: eps must be > 0");
+    require(c->state[c->cur].count == c->ncell, "state count must equal the mesh cell count");
+    cudaSetDevice(c->device);
+    build_step_terms(c);
+    reset_counters(c);
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaEventRecord(a, c->st));
+    for (int k = 0; k < nsteps; ++k) step_once(c, dt, eps, cap);
+    CK(cudaEventRecord(b, c->st));
+    CK(cudaEventSynchronize(b));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (ms) *ms = f;
+  });
+}
+
+int ttdvm_cuda_fp64_peak(ttdvm_ctx* c, double* tflops) {
+  return guard(c, [&] {
+    cudaSetDevice(c->device);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    const int threads = 512, blocks = sms * 4, iters = 4000;
+    DevBuf<double> out;
+    out.alloc(blocks);
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(launch_dfma_probe(out.p, blocks, threads, 100, c->st));  // warm-up
+    CK(cudaEventRecord(a, c->st));
+    CK(launch_dfma_probe(out.p, blocks, threads, iters, c->st));
+    CK(cudaEventRecord(b, c->st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    out.free();
+    const double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+  });
+}
+
+int64_t ttdvm_cuda_launch_count(const ttdvm_ctx* c) { return c ? c->launches : -1; }
+
+int ttdvm_cuda_set_profiling(ttdvm_ctx* c, int on) {
+  return guard(c, [&] { c->profiling = on != 0; });
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// Shared device-side types of the TT-DVM CUDA library (sm_100a, FP64).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ttdvm {
+
+constexpr int kMaxSets = 8;
+constexpr int kMaxTerms = 16;     // summands per rounded output
+constexpr int kRoundThreads = 256;
+
+// A set of packed TT tensors (ttdvm_tt_batch layout) resident in an arena.
+struct TSet {
+  const int* ranks;        // [2*count]
+  const long long* off;    // [count]
+  const double* base;
+  const double* tscale;    // optional per-tensor scale (e.g. nu of J)
+  double uscale;           // uniform scale (e.g. dt for R)
+};
+
+// One summand of a rounded output: scale * (factor o reflect(set[idx])).
+// factor (>= 0) indexes a rank-1 face factor u1 (x) u2 (x) u3 in
+// RoundArgs::factors (the axis-aligned (xi.n)^{+/-});
+// refl (1..3) is the specular-ghost index reversal (T9 / T20).
+struct Term {
+  int set;
+  int idx;
+  double scale;
+  int fac;
+  int refl;
+};
+
+struct RoundOut {
+  int* ranks;                   // [2*nout]
+  long long* off;               // [nout]
+  double* base;
+  unsigned long long* used;     // bump counter (doubles)
+  long long capacity;           // doubles
+};
+
+// status words written by kernels (device memory, read back by the host)
+enum StatusWord {
+  kStOverflow = 0,  // an output did not fit its arena
+  kStMaxR1 = 1,
+  kStMaxR2 = 2,
+  kStError = 3,     // 0 ok, else error code (see kErr*)
+  kStErrIdx = 4,    // index of the first failing item
+  kStWords = 8
+};
+enum ErrCode { kErrNone = 0, kErrDensity = 1, kErrTemperature = 2, kErrNonFinite = 3 };
+
+struct RoundArgs {
+  TSet sets[kMaxSets];
+  const long long* term_off;    // [nout+1] CSR into terms
+  const Term* terms;
+  const double* factors;        // [nfac][n1+n2+n3]
+  int n1, n2, n3;
+  int nout;
+  double eps;
+  int cap;
+  RoundOut out;
+  int* status;                  // [kStWords]
+  double* margins;              // optional [2*nout]
+  double* acc;                  // [2]: canonical FLOPs, compulsory bytes (atomicAdd)
+  // shared-memory plan (doubles), chosen by the host launcher
+  int RM1, RM2;                 // bounds on the summed input ranks
+  int HMAX;                     // rows of the TSQR block buffer
+};
+
+}  // namespace ttdvm

@@ -1,0 +1,285 @@
+"""ctypes binding of libttdvm_cuda.so -- the host-side mirror of the
+reference's TT / physics / step interface over the C ABI
+(include/ttdvm_cuda.h).
+
+Names follow the reference: ``rounded`` (TtTensor::rounded,
+proj/src/tt_tensor.cpp:139-193), ``compute_macro`` (physics.cpp:17-67),
+``compute_collision`` (physics.cpp:112-125) and ``explicit_step`` (the step
+SPEC.md:391 declares).  Errors map like the reference's exceptions:
+TTDVM_EINVAL -> ValueError (std::invalid_argument), TTDVM_EDOMAIN ->
+RuntimeError (std::runtime_error).  There is no CPU fallback: without the
+built library or a GPU every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .tt_batch import TtBatch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libttdvm_cuda.so")
+
+# every symbol declared in include/ttdvm_cuda.h
+EXPORTS = (
+    "ttdvm_cuda_create", "ttdvm_cuda_destroy", "ttdvm_cuda_last_error", "ttdvm_cuda_set_grid",
+    "ttdvm_cuda_set_gas", "ttdvm_cuda_set_mesh", "ttdvm_cuda_set_bcs", "ttdvm_cuda_upload_state",
+    "ttdvm_cuda_state_layout", "ttdvm_cuda_download_state", "ttdvm_cuda_step",
+    "ttdvm_cuda_macros", "ttdvm_cuda_stage_layout", "ttdvm_cuda_stage_download",
+    "ttdvm_cuda_round_batch", "ttdvm_cuda_result_layout", "ttdvm_cuda_result_download",
+    "ttdvm_cuda_macro_batch", "ttdvm_cuda_collision_batch", "ttdvm_cuda_phase_times",
+    "ttdvm_cuda_launch_count", "ttdvm_cuda_set_profiling", "ttdvm_cuda_phase_work",
+    "ttdvm_cuda_timed_step", "ttdvm_cuda_fp64_peak",
+)
+
+OK, EINVAL, EDOMAIN, ENOMEM, ECUDA, ENCCL = range(6)
+BC_KIND = {"wall": 0, "sym-x": 1, "sym-y": 2, "sym-z": 3, "in": 4, "out": 5}
+STAGE = {"phi": 0, "jr": 1, "res": 2, "fs": 3}
+
+
+class TtBatchC(C.Structure):
+    _fields_ = [("count", C.c_int32), ("n1", C.c_int32), ("n2", C.c_int32), ("n3", C.c_int32),
+                ("ranks", C.c_void_p), ("offsets", C.c_void_p), ("cores", C.c_void_p)]
+
+
+class BcC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("wall_temperature", C.c_double), ("free_n", C.c_double),
+                ("free_t", C.c_double), ("free_u", C.c_double * 3)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load the in-tree library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: run `python -m paper_1912_04582_b200.build` "
+                          "(the product path has no CPU fallback)")
+    lib = C.CDLL(path)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    sig = {
+        "ttdvm_cuda_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+        "ttdvm_cuda_destroy": (C.c_int, [vp]),
+        "ttdvm_cuda_last_error": (C.c_char_p, [vp]),
+        "ttdvm_cuda_set_grid": (C.c_int, [vp, C.c_int, dbl]),
+        "ttdvm_cuda_set_gas": (C.c_int, [vp, vp]),
+        "ttdvm_cuda_set_mesh": (C.c_int, [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "ttdvm_cuda_set_bcs": (C.c_int, [vp, i32, vp]),
+        "ttdvm_cuda_upload_state": (C.c_int, [vp, vp]),
+        "ttdvm_cuda_state_layout": (C.c_int, [vp, vp, vp]),
+        "ttdvm_cuda_download_state": (C.c_int, [vp, vp, i64]),
+        "ttdvm_cuda_step": (C.c_int, [vp, dbl, dbl, i32, i32]),
+        "ttdvm_cuda_macros": (C.c_int, [vp, vp]),
+        "ttdvm_cuda_stage_layout": (C.c_int, [vp, i32, vp, vp, vp]),
+        "ttdvm_cuda_stage_download": (C.c_int, [vp, i32, vp, i64]),
+        "ttdvm_cuda_round_batch": (C.c_int, [vp, vp, i32, vp, vp, dbl, i32, vp]),
+        "ttdvm_cuda_result_layout": (C.c_int, [vp, vp, vp]),
+        "ttdvm_cuda_result_download": (C.c_int, [vp, vp, i64]),
+        "ttdvm_cuda_macro_batch": (C.c_int, [vp, vp, vp]),
+        "ttdvm_cuda_collision_batch": (C.c_int, [vp, vp, dbl, vp]),
+        "ttdvm_cuda_phase_times": (C.c_int, [vp, vp]),
+        "ttdvm_cuda_launch_count": (C.c_int64, [vp]),
+        "ttdvm_cuda_set_profiling": (C.c_int, [vp, C.c_int]),
+        "ttdvm_cuda_phase_work": (C.c_int, [vp, vp, vp, vp]),
+        "ttdvm_cuda_timed_step": (C.c_int, [vp, dbl, dbl, i32, i32, vp]),
+        "ttdvm_cuda_fp64_peak": (C.c_int, [vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _batch_struct(b: TtBatch):
+    s = TtBatchC(b.count, b.n1, b.n2, b.n3, _ptr(b.ranks), _ptr(b.offsets), _ptr(b.cores))
+    return s
+
+
+class Context:
+    """One CUDA context of the TT-DVM step (one per GPU / rank)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        rc = self.lib.ttdvm_cuda_create(int(device), C.byref(h))
+        if rc != OK:
+            raise RuntimeError(f"ttdvm_cuda_create failed (code {rc}): no usable CUDA device")
+        self.h = h
+        self.n = 0
+        self.mesh = None
+
+    # -- plumbing -------------------------------------------------------------
+    def _check(self, rc: int):
+        if rc == OK:
+            return
+        msg = self.lib.ttdvm_cuda_last_error(self.h).decode()
+        if rc == EINVAL:
+            raise ValueError(msg)
+        if rc == EDOMAIN:
+            raise RuntimeError(msg)
+        if rc == ENOMEM:
+            raise MemoryError(msg)
+        raise RuntimeError(f"CUDA error: {msg}")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ttdvm_cuda_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- set-up ------------------------------------------------------------------
+    def set_grid(self, n: int, bound: float):
+        self._check(self.lib.ttdvm_cuda_set_grid(self.h, int(n), float(bound)))
+        self.n = int(n)
+
+    def set_gas(self, gas):
+        g = np.ascontiguousarray(gas, dtype=np.float64)
+        self._check(self.lib.ttdvm_cuda_set_gas(self.h, _ptr(g)))
+
+    def set_mesh(self, m):
+        self.mesh = m
+        self._keep = [m.face_left, m.face_right, m.face_group, m.face_area, m.face_normal,
+                      m.cell_volume, m.cell_face_off, m.cell_face_id, m.cell_face_sign]
+        self._check(self.lib.ttdvm_cuda_set_mesh(
+            self.h, m.ncell, m.nface, *(_ptr(np.ascontiguousarray(a)) for a in self._keep)))
+
+    def set_bcs(self, bcs):
+        arr = (BcC * max(1, len(bcs)))()
+        for g, bc in enumerate(bcs):
+            arr[g].kind = BC_KIND[bc["kind"]]
+            arr[g].wall_temperature = float(bc.get("t_wall", 0.0))
+            arr[g].free_n = float(bc.get("n", 0.0))
+            arr[g].free_t = float(bc.get("t", 0.0))
+            u = bc.get("u", (0.0, 0.0, 0.0))
+            for a in range(3):
+                arr[g].free_u[a] = float(u[a])
+        self._check(self.lib.ttdvm_cuda_set_bcs(self.h, len(bcs), C.cast(arr, C.c_void_p)))
+
+    def setup(self, problem):
+        self.set_grid(problem.nv, problem.bound)
+        self.set_gas(problem.gas)
+        self.set_mesh(problem.mesh)
+        self.set_bcs(problem.bcs)
+        self.upload_state(problem.f0)
+
+    # -- state ---------------------------------------------------------------------
+    def upload_state(self, b: TtBatch):
+        s = _batch_struct(b)
+        self._check(self.lib.ttdvm_cuda_upload_state(self.h, C.byref(s)))
+
+    def _fetch(self, count, layout_fn, download_fn) -> TtBatch:
+        ranks = np.zeros(2 * max(count, 1), dtype=np.int32)
+        offs = np.zeros(count + 1, dtype=np.int64)
+        self._check(layout_fn(_ptr(ranks), _ptr(offs)))
+        cores = np.zeros(max(1, int(offs[count])), dtype=np.float64)
+        self._check(download_fn(_ptr(cores), int(cores.size)))
+        return TtBatch(self.n, self.n, self.n, ranks[:2 * count], offs, cores[:int(offs[count])])
+
+    def download_state(self) -> TtBatch:
+        count = self.mesh.ncell
+        return self._fetch(count,
+                           lambda r, o: self.lib.ttdvm_cuda_state_layout(self.h, r, o),
+                           lambda c, cap: self.lib.ttdvm_cuda_download_state(self.h, c, cap))
+
+    def stage(self, name: str) -> TtBatch:
+        sid = STAGE[name]
+        cnt = C.c_int32()
+        self._check(self.lib.ttdvm_cuda_stage_layout(self.h, sid, C.byref(cnt), None, None))
+        count = cnt.value
+        return self._fetch(count,
+                           lambda r, o: self.lib.ttdvm_cuda_stage_layout(self.h, sid, None, r, o),
+                           lambda c, cap: self.lib.ttdvm_cuda_stage_download(self.h, sid, c, cap))
+
+    # -- the hot path ----------------------------------------------------------------
+    def step(self, dt: float, eps: float, cap: int = 0, nsteps: int = 1):
+        """explicit_step, nsteps times, state resident."""
+        self._check(self.lib.ttdvm_cuda_step(self.h, float(dt), float(eps), int(cap), int(nsteps)))
+
+    def macros(self) -> np.ndarray:
+        out = np.zeros((self.mesh.ncell, 11))
+        self._check(self.lib.ttdvm_cuda_macros(self.h, _ptr(out)))
+        return out
+
+    def rounded(self, b: TtBatch, eps: float, cap: int = 0, group_off=None, scale=None,
+                margins: bool = False):
+        """Batched TtTensor::rounded of (optionally grouped, scaled) sums."""
+        s = _batch_struct(b)
+        nout = b.count if group_off is None else len(group_off) - 1
+        go = None if group_off is None else np.ascontiguousarray(group_off, dtype=np.int64)
+        sc = None if scale is None else np.ascontiguousarray(scale, dtype=np.float64)
+        mg = np.zeros(2 * max(nout, 1)) if margins else None
+        self._check(self.lib.ttdvm_cuda_round_batch(self.h, C.byref(s), nout, _ptr(go), _ptr(sc),
+                                                    float(eps), int(cap), _ptr(mg)))
+        out = self._fetch(nout, lambda r, o: self.lib.ttdvm_cuda_result_layout(self.h, r, o),
+                          lambda c, cap_: self.lib.ttdvm_cuda_result_download(self.h, c, cap_))
+        if margins:
+            return out, mg[:2 * nout].reshape(nout, 2)
+        return out
+
+    def compute_macro(self, b: TtBatch) -> np.ndarray:
+        """Batched compute_macro: [count, 11] = n, u(3), T, rho, p, S(3), nu."""
+        s = _batch_struct(b)
+        out = np.zeros((max(b.count, 1), 11))
+        self._check(self.lib.ttdvm_cuda_macro_batch(self.h, C.byref(s), _ptr(out)))
+        return out[:b.count]
+
+    def compute_collision(self, b: TtBatch, eps: float):
+        """Batched compute_collision: returns (J_r = round(f_S - f), macros);
+        J = nu * J_r with nu = macros[:, 10] (physics.cpp:118)."""
+        s = _batch_struct(b)
+        mac = np.zeros((max(b.count, 1), 11))
+        self._check(self.lib.ttdvm_cuda_collision_batch(self.h, C.byref(s), float(eps), _ptr(mac)))
+        jr = self._fetch(b.count, lambda r, o: self.lib.ttdvm_cuda_result_layout(self.h, r, o),
+                         lambda c, cap: self.lib.ttdvm_cuda_result_download(self.h, c, cap))
+        return jr, mac[:b.count]
+
+    def phase_times(self) -> np.ndarray:
+        out = np.zeros(8)
+        self._check(self.lib.ttdvm_cuda_phase_times(self.h, _ptr(out)))
+        return out
+
+    def timed_step(self, dt: float, eps: float, cap: int = 0, nsteps: int = 1) -> float:
+        """Step nsteps times; returns device ms (CUDA events on the library stream)."""
+        ms = np.zeros(1)
+        self._check(self.lib.ttdvm_cuda_timed_step(self.h, float(dt), float(eps), int(cap),
+                                                   int(nsteps), _ptr(ms)))
+        return float(ms[0])
+
+    def phase_work(self):
+        fl, by = np.zeros(8), np.zeros(8)
+        la = np.zeros(8, dtype=np.int32)
+        self._check(self.lib.ttdvm_cuda_phase_work(self.h, _ptr(fl), _ptr(by), _ptr(la)))
+        return fl, by, la
+
+    def fp64_peak(self) -> float:
+        """Measured DFMA peak in TFLOP/s."""
+        t = np.zeros(1)
+        self._check(self.lib.ttdvm_cuda_fp64_peak(self.h, _ptr(t)))
+        return float(t[0])
+
+    def launch_count(self) -> int:
+        return int(self.lib.ttdvm_cuda_launch_count(self.h))
+
+    def set_profiling(self, on: bool):
+        self._check(self.lib.ttdvm_cuda_set_profiling(self.h, 1 if on else 0))
+
+
+def explicit_step(ctx: Context, dt: float, eps: float, cap: int = 0, nsteps: int = 1):
+    """SPEC.md:391's explicit_step over the resident state of ``ctx``."""
+    ctx.step(dt, eps, cap, nsteps)
