@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "ttdvm_cuda.h")).read()
-    return sorted(set(re.findall(r"\b(ttdvm_cuda_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(ttdvm_cuda_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_and_binding_agree():
