@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     return ap.parse_args()
 
 
@@ -201,6 +201,8 @@ def run_reference(args):
 # ------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
+    if args.e2e_steps <= 0:
+        args.e2e_steps = args.steps
     if args.impl == "reference":
         run_reference(args)
         return
@@ -243,17 +245,20 @@ def main():
     # e2e through the public API with host buffers: upload state, one step,
     # download state -- every step
     ctx.set_profiling(False)
+    # (the host state advances: steps 1..E from the initial state, as timed)
     host = p.f0
-    h2d = int(host.cores.nbytes + host.ranks.nbytes + host.offsets.nbytes)
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
-    d2h = 0
+    h2d = d2h = 0
     for _ in range(args.e2e_steps):
+        h2d += int(host.cores.nbytes + host.ranks.nbytes + host.offsets.nbytes)
         ctx.upload_state(host)
         ctx.step(p.dt, p.eps, p.cap, 1)
-        host_out = ctx.download_state()
-        d2h = int(host_out.cores.nbytes + host_out.ranks.nbytes + host_out.offsets.nbytes)
+        host = ctx.download_state()
+        d2h += int(host.cores.nbytes + host.ranks.nbytes + host.offsets.nbytes)
+    h2d //= args.e2e_steps
+    d2h //= args.e2e_steps
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist:

@@ -143,6 +143,9 @@ int ttdvm_cuda_timed_step(ttdvm_ctx* ctx, double dt, double eps, int32_t cap, in
 /* Measured FP64 FMA peak of this device (TFLOP/s), the roofline
  * denominator of the FP64-bound rounding kernels. */
 int ttdvm_cuda_fp64_peak(ttdvm_ctx* ctx, double* tflops);
+/* Diagnostics: per-phase SM cycles (thread 0 of every CTA, summed) of the
+ * rounding kernel since the previous call; on != 0 keeps collecting. */
+int ttdvm_cuda_round_profile(ttdvm_ctx* ctx, int on, uint64_t* cycles16);
 /* Number of kernel launches issued by the last call. */
 int64_t ttdvm_cuda_launch_count(const ttdvm_ctx* ctx);
 /* Enable/disable per-phase CUDA-event timing (costs one sync per phase). */

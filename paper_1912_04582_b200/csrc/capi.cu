@@ -23,7 +23,8 @@
 
 namespace ttdvm {
 cudaError_t launch_round(const RoundArgs& a, cudaStream_t st);
-size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX);
+cudaError_t launch_round_bounds(const RoundArgs& a, int* bounds, cudaStream_t st);
+size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int MSMAX);
 struct MacroArgs {
   TSet set;
   int count, n;
@@ -181,6 +182,8 @@ struct ttdvm_ctx {
   double phase_flops[8] = {0}, phase_bytes[8] = {0};
   int phase_launches[8] = {0};
   DevBuf<double> d_acc;
+  DevBuf<unsigned long long> d_prof;  // per-phase cycles of the rounding kernel
+  bool round_prof = false;
   int cur_phase = 7;
   long long launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -284,58 +287,59 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   if (nout == 0) return;
   require(tl.maxk <= kMaxTerms, "too many summands per rounded output");
   ensure_static(c);
-  // rank bounds: sum over the summands of the set maxima
-  int RM1 = 1, RM2 = 1;
-  {
-    // per-output term count is small; bound with maxk * max over sets used
-    int m1 = 1, m2 = 1;
-    for (const Term& t : tl.terms) {
-      m1 = std::max(m1, sets[t.set]->maxr1);
-      m2 = std::max(m2, sets[t.set]->maxr2);
-    }
-    RM1 = std::max(1, tl.maxk * m1);
-    RM2 = std::max(1, tl.maxk * m2);
-  }
   const int n = c->n;
+  RoundArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int s = 0; s < kMaxSets; ++s)
+    if (sets[s]) a.sets[s] = sets[s]->view();
+  a.term_off = tl.d_off.p;
+  a.terms = tl.d_terms.p;
+  a.factors = c->d_factors.p;
+  a.n1 = a.n2 = a.n3 = n;
+  a.nout = nout;
+  a.eps = eps;
+  a.cap = cap;
+  a.status = c->d_status.p;
+  a.margins = margins_dev;
+  a.acc = c->d_acc.p;
+  a.prof = c->round_prof ? c->d_prof.p : nullptr;
+  // exact per-launch bounds of the summed ranks (one tiny kernel + readback)
+  CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
+  CK(launch_round_bounds(a, c->d_status.p, c->st));
+  c->launches += 1;
+  CK(cudaMemcpyAsync(c->h_status, c->d_status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const int RM1 = std::max(1, c->h_status[0]);
+  const int RM2 = std::max(1, c->h_status[1]);
+  const int MSMAX = std::max(1, c->h_status[2]);
   const int mx = n;
+  // TSQR block height: as tall as the shared-memory budget allows, aiming
+  // at >= 3 resident CTAs per SM
   int HMAX = std::max(mx, std::min(4 * mx, 128));
-  size_t smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX);
-  while (smem > 227 * 1024 && HMAX > mx) {
-    HMAX = std::max(mx, HMAX / 2);
-    smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX);
+  size_t smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX, MSMAX);
+  while (smem > 75 * 1024 && HMAX > mx) {
+    HMAX = std::max(mx, HMAX - mx);
+    smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX, MSMAX);
   }
   if (smem > 227 * 1024)
     throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory (n=" + std::to_string(n) +
                                  ", summed ranks " + std::to_string(RM1) + "x" +
                                  std::to_string(RM2) + ")"};
+  a.RM1 = RM1;
+  a.RM2 = RM2;
+  a.HMAX = HMAX;
+  a.MSMAX = MSMAX;
   // arena estimate
   if (out.arena.n == 0) {
     const int re = std::min(n, std::max(8, std::max(RM1, RM2) / std::max(1, tl.maxk) + 4));
     out.arena.alloc((size_t)nout * tt_size(n, n, n, re, re) + 1024);
   }
   for (int attempt = 0; attempt < 8; ++attempt) {
-    RoundArgs a;
-    memset(&a, 0, sizeof(a));
-    for (int s = 0; s < kMaxSets; ++s)
-      if (sets[s]) a.sets[s] = sets[s]->view();
-    a.term_off = tl.d_off.p;
-    a.terms = tl.d_terms.p;
-    a.factors = c->d_factors.p;
-    a.n1 = a.n2 = a.n3 = n;
-    a.nout = nout;
-    a.eps = eps;
-    a.cap = cap;
     a.out.ranks = out.ranks.p;
     a.out.off = out.off.p;
     a.out.base = out.arena.p;
     a.out.used = reinterpret_cast<unsigned long long*>(c->d_status.p + kStWords);
     a.out.capacity = (long long)out.arena.n;
-    a.status = c->d_status.p;
-    a.margins = margins_dev;
-    a.acc = c->d_acc.p;
-    a.RM1 = RM1;
-    a.RM2 = RM2;
-    a.HMAX = HMAX;
     CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
     CK(cudaMemsetAsync(c->d_acc.p, 0, 2 * sizeof(double), c->st));
     CK(launch_round(a, c->st));
@@ -679,6 +683,7 @@ int ttdvm_cuda_destroy(ttdvm_ctx* c) {
   c->d_nu.free();
   c->d_status.free();
   c->d_acc.free();
+  c->d_prof.free();
   c->d_margins.free();
   c->d_tmp.free();
   c->d_tmp_off.free();
@@ -940,6 +945,15 @@ int ttdvm_cuda_timed_step(ttdvm_ctx* c, double dt, double eps, int32_t cap, int3
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     if (ms) *ms = f;
+  });
+}
+
+int ttdvm_cuda_round_profile(ttdvm_ctx* c, int on, uint64_t* cycles16) {
+  return guard(c, [&] {
+    c->d_prof.alloc(16);
+    if (cycles16) CK(cudaMemcpy(cycles16, c->d_prof.p, 16 * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(c->d_prof.p, 0, 16 * 8));
+    c->round_prof = on != 0;
   });
 }
 

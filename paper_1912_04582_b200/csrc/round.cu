@@ -1,6 +1,6 @@
 // Batched FP64 TT rounding of implicit sums.
 //
-// One CTA (256 threads) owns one output tensor.  Its input is a list of
+// One CTA (128 threads) owns one output tensor.  Its input is a list of
 // summands (Term) -- scaled, optionally face-factor-weighted and reflected
 // TT tensors read straight from their arenas -- so the rank-inflated sum of
 // a face flux, cell residual or update is never materialised
@@ -16,14 +16,17 @@
 //      the stacked (F M_j R3^T)^T).  Both tall QRs run as a TSQR over
 //      slices j with a structured Householder update of the running R
 //      (only R is needed, never the tall Q).
-//   3. One-sided Jacobi SVD of C -> sigma_1, U1; budget eps^2 ||A||^2 / 2
-//      (reference :167-169); truncation_rank (reference :18-29).
-//   4. Cut 2: S_j = (U1^T F) M_j R3^T, TSQR of the stacked S_j -> R_S,
-//      Jacobi SVD with V -> sigma_2, V2; truncation_rank.
-//   5. Output first = U1, middle_j = S_j V2, last = (Q3 V2)^T.
-// All arithmetic FP64.  Reconstructions equal the reference's up to
-// roundoff; cores differ by the usual orthogonal gauge (the reference puts
-// Sigma_2 into last, here it sits in middle).
+//   3. SVD of C: column-pivoted QR of C^T, then one-sided Jacobi on R^T
+//      (Drmac-Veselic preconditioning: ~5 sweeps instead of ~12), which
+//      yields sigma_1 and U1 without accumulating rotations; budget
+//      eps^2 ||A||^2 / 2 (reference :167-169); truncation_rank (:18-29).
+//   4. Cut 2: S_j = (U1^T F) M_j R3^T, TSQR of the stacked S_j -> R_S, the
+//      same SVD on R_S^T -> sigma_2 and the right vectors V2.
+//   5. Output first = U1, middle_j = (U1^T F) M_j (R3^T V2), last = (Q3 V2)^T.
+// The middle slices of all summands for the current j are staged in shared
+// memory once per use.  All arithmetic FP64.  Reconstructions equal the
+// reference's up to roundoff; cores differ by an orthogonal gauge (the
+// reference keeps Sigma_2 in last, here it sits in middle).
 #include <math.h>
 
 #include "ttdvm_device.cuh"
@@ -39,7 +42,7 @@ struct TermInfo {
   const double* base;
   const double* u[3];
   double scale;
-  int r1, r2, off1, off2, refl;
+  int r1, r2, off1, off2, refl, ms;
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -93,7 +96,6 @@ __device__ __forceinline__ int floor_pow2(int x) {
 __device__ void qr_inplace(double* A, int lda, int m, int ncols, double* tau, double* sh) {
   const int kmax = min(m, ncols);
   for (int k = 0; k < kmax; ++k) {
-    // sigma2 = ||A[k+1:m, k]||^2 by warp 0
     if (threadIdx.x < 32) {
       double s = 0.0;
       for (int i = k + 1 + threadIdx.x; i < m; i += 32) s += A[i + lda * k] * A[i + lda * k];
@@ -132,13 +134,12 @@ __device__ void qr_inplace(double* A, int lda, int m, int ncols, double* tau, do
 }
 
 // QR of [R; B] -> R, R upper c x c (ld ldr), B h x c (ld ldb); B destroyed.
-// Threads: groups of tpc lanes per column, rows strided inside the group.
+// Threads: groups of TPC lanes per column, rows strided inside the group.
 template <int TPC>
 __device__ void qr_update_t(double* R, int ldr, double* B, int ldb, int h, int c, double* sh) {
   const int g = threadIdx.x / TPC, sub = threadIdx.x % TPC;
   const int ngroups = NT / TPC;
-  // sigma2 of column 0 (all of warp 0 reaches the shuffles)
-  if (threadIdx.x < 32) {
+  if (threadIdx.x < 32) {  // sigma2 of column 0 (all of warp 0 reaches the shuffles)
     double s = 0.0;
     if (g == 0)
       for (int i = sub; i < h; i += TPC) s += B[i] * B[i];
@@ -150,14 +151,12 @@ __device__ void qr_update_t(double* R, int ldr, double* B, int ldb, int h, int c
     double beta, t, sc;
     larfg(R[k + ldr * k], sh[k & 1], beta, t, sc);
     if (t != 0.0) {
-      // the group owning column k scales v (groups are assigned l - k - 1)
       for (int i = threadIdx.x; i < h; i += NT) B[i + ldb * k] *= sc;
     }
     __syncthreads();
     if (threadIdx.x == 0 && t != 0.0) R[k + ldr * k] = beta;
     const double* v = B + ldb * k;
-    // uniform trip count across the block: every lane reaches the shuffles
-    for (int base = k + 1; base < c; base += ngroups) {
+    for (int base = k + 1; base < c; base += ngroups) {  // uniform trip count
       const int l = base + g;
       const bool act = l < c;
       double* col = B + ldb * (act ? l : k);
@@ -196,16 +195,112 @@ __device__ void qr_update(double* R, int ldr, double* B, int ldb, int h, int c, 
   }
 }
 
-// One-sided (Hestenes) Jacobi SVD of A (m x c, ld lda) in place: on exit
-// the columns of A are U*Sigma (unsorted) and V (c x c, ld ldv, optional,
-// must hold the identity on entry) accumulates the rotations.
+// Column-pivoted Householder QR of M (p x m, ld ldm) in place (dgeqp3
+// semantics, Q discarded): on exit the upper trapezoid holds R (k x m,
+// k = min(p, m)) of M Pi, piv[i] = original column at position i.
+__device__ void qrp_inplace(double* M, int ldm, int p, int m, double* vn, int* piv, double* sh) {
+  const int kmax = min(p, m);
+  for (int j = threadIdx.x; j < m; j += NT) {
+    double s = 0.0;
+    for (int i = 0; i < p; ++i) s += M[i + ldm * j] * M[i + ldm * j];
+    vn[j] = s;
+    piv[j] = j;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < kmax; ++k) {
+    // argmax_{j >= k} vn[j], computed redundantly by every warp
+    double bv = -1.0;
+    int bi = k;
+    for (int j = k + lane; j < m; j += 32) {
+      const double v = vn[j];
+      if (v > bv) {
+        bv = v;
+        bi = j;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    const int pv = bi;
+    __syncthreads();  // everyone has read vn
+    if (pv != k) {
+      for (int i = threadIdx.x; i < p; i += NT) {
+        const double a = M[i + ldm * k];
+        M[i + ldm * k] = M[i + ldm * pv];
+        M[i + ldm * pv] = a;
+      }
+      if (threadIdx.x == 0) {
+        const double a = vn[k];
+        vn[k] = vn[pv];
+        vn[pv] = a;
+        const int q = piv[k];
+        piv[k] = piv[pv];
+        piv[pv] = q;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double s = 0.0;
+      for (int i = k + 1 + threadIdx.x; i < p; i += 32) s += M[i + ldm * k] * M[i + ldm * k];
+      s = warp_sum(s);
+      if (threadIdx.x == 0) {
+        double beta, t, sc;
+        larfg(M[k + ldm * k], s, beta, t, sc);
+        sh[0] = t;
+        sh[1] = sc;
+        sh[2] = beta;
+      }
+    }
+    __syncthreads();
+    const double t = sh[0], sc = sh[1];
+    for (int l = k + 1 + threadIdx.x; l < m; l += NT) {
+      double* col = M + ldm * l;
+      double s = 0.0;
+      if (t != 0.0) {
+        const double* v = M + ldm * k;
+        double w = col[k];
+        for (int i = k + 1; i < p; ++i) w += (v[i] * sc) * col[i];
+        w *= t;
+        col[k] -= w;
+        for (int i = k + 1; i < p; ++i) {
+          const double x = col[i] - w * (v[i] * sc);
+          col[i] = x;
+          s += x * x;
+        }
+      } else {
+        for (int i = k + 1; i < p; ++i) s += col[i] * col[i];
+      }
+      vn[l] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && t != 0.0) M[k + ldm * k] = sh[2];
+    __syncthreads();
+  }
+}
+
+// One-sided (Hestenes) Jacobi on the columns of X (m x c, ld ldx) with
+// tracked squared column norms (one dot product per pair and round; the
+// norms are refreshed at every sweep).
 template <int TPP>
-__device__ void jacobi_t(double* A, int lda, int m, int c, double* V, int ldv, int* flag) {
+__device__ void jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
   const int cp = c + (c & 1);
   const int npairs = cp / 2;
   const int pi = threadIdx.x / TPP, sub = threadIdx.x % TPP;
   const double tol = 1e-15;
   for (int sweep = 0; sweep < 60; ++sweep) {
+    for (int j = threadIdx.x; j < c; j += NT) {
+      double s = 0.0;
+      for (int i = 0; i < m; ++i) s += X[i + ldx * j] * X[i + ldx * j];
+      nrm[j] = s;
+    }
+    __syncthreads();
     bool rotated = false;
     for (int r = 0; r < cp - 1; ++r) {
       for (int base = 0; base < npairs; base += NT / TPP) {
@@ -213,42 +308,32 @@ __device__ void jacobi_t(double* A, int lda, int m, int c, double* V, int ldv, i
         const int a = pp == 0 ? 0 : ((pp + r - 1) % (cp - 1)) + 1;
         const int b = ((cp - 1 - pp + r - 1) % (cp - 1)) + 1;
         const bool live = pp < npairs && a < c && b < c;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        double* x = A + lda * (live ? a : 0);
-        double* y = A + lda * (live ? b : 0);
-        if (live) {
-          for (int i = sub; i < m; i += TPP) {
-            const double xi = x[i], yi = y[i];
-            al += xi * xi;
-            be += yi * yi;
-            ga += xi * yi;
-          }
-        }
-        al = group_sum<TPP>(al);
-        be = group_sum<TPP>(be);
+        double ga = 0.0;
+        double* x = X + ldx * (live ? a : 0);
+        double* y = X + ldx * (live ? b : 0);
+        if (live)
+          for (int i = sub; i < m; i += TPP) ga += x[i] * y[i];
         ga = group_sum<TPP>(ga);
-        if (live && ga != 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
-          rotated = true;
-          const double zeta = (be - al) / (2.0 * ga);
-          double t;
-          if (fabs(zeta) > 1e150) {
-            t = 0.5 / zeta;
-          } else {
-            t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          }
-          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-          for (int i = sub; i < m; i += TPP) {
-            const double xi = x[i], yi = y[i];
-            x[i] = cs * xi - sn * yi;
-            y[i] = sn * xi + cs * yi;
-          }
-          if (V) {
-            double* vx = V + ldv * a;
-            double* vy = V + ldv * b;
-            for (int i = sub; i < c; i += TPP) {
-              const double xi = vx[i], yi = vy[i];
-              vx[i] = cs * xi - sn * yi;
-              vy[i] = sn * xi + cs * yi;
+        if (live && ga != 0.0) {
+          const double al = nrm[a], be = nrm[b];
+          if (fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+            rotated = true;
+            const double zeta = (be - al) / (2.0 * ga);
+            double t;
+            if (fabs(zeta) > 1e150) {
+              t = 0.5 / zeta;
+            } else {
+              t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            }
+            const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+            for (int i = sub; i < m; i += TPP) {
+              const double xi = x[i], yi = y[i];
+              x[i] = cs * xi - sn * yi;
+              y[i] = sn * xi + cs * yi;
+            }
+            if (sub == 0) {
+              nrm[a] = al - t * ga;
+              nrm[b] = be + t * ga;
             }
           }
         }
@@ -257,42 +342,19 @@ __device__ void jacobi_t(double* A, int lda, int m, int c, double* V, int ldv, i
     }
     if (!__syncthreads_or(rotated ? 1 : 0)) break;
   }
-  (void)flag;
 }
 
-__device__ void jacobi(double* A, int lda, int m, int c, double* V, int ldv) {
+__device__ void jacobi(double* X, int ldx, int m, int c, double* nrm) {
   const int npairs = (c + 1) / 2;
   const int tpp = min(32, floor_pow2(max(1, NT / max(npairs, 1))));
   switch (tpp) {
-    case 32: jacobi_t<32>(A, lda, m, c, V, ldv, nullptr); break;
-    case 16: jacobi_t<16>(A, lda, m, c, V, ldv, nullptr); break;
-    case 8: jacobi_t<8>(A, lda, m, c, V, ldv, nullptr); break;
-    case 4: jacobi_t<4>(A, lda, m, c, V, ldv, nullptr); break;
-    case 2: jacobi_t<2>(A, lda, m, c, V, ldv, nullptr); break;
-    default: jacobi_t<1>(A, lda, m, c, V, ldv, nullptr); break;
+    case 32: jacobi_t<32>(X, ldx, m, c, nrm); break;
+    case 16: jacobi_t<16>(X, ldx, m, c, nrm); break;
+    case 8: jacobi_t<8>(X, ldx, m, c, nrm); break;
+    case 4: jacobi_t<4>(X, ldx, m, c, nrm); break;
+    case 2: jacobi_t<2>(X, ldx, m, c, nrm); break;
+    default: jacobi_t<1>(X, ldx, m, c, nrm); break;
   }
-}
-
-// Column norms of A (m x c) -> sig sorted descending with perm.
-__device__ void sorted_norms(const double* A, int lda, int m, int c, double* sig_raw, double* sig,
-                             int* perm) {
-  for (int p = threadIdx.x; p < c; p += NT) {
-    double s = 0.0;
-    for (int i = 0; i < m; ++i) s += A[i + lda * p] * A[i + lda * p];
-    sig_raw[p] = sqrt(s);
-  }
-  __syncthreads();
-  for (int p = threadIdx.x; p < c; p += NT) {
-    const double v = sig_raw[p];
-    int rank = 0;
-    for (int q = 0; q < c; ++q) {
-      const double w = sig_raw[q];
-      rank += (w > v) || (w == v && q < p);
-    }
-    sig[rank] = v;
-    perm[rank] = p;
-  }
-  __syncthreads();
 }
 
 // proj/src/tt_tensor.cpp:18-29, plus the decision margin.
@@ -316,6 +378,59 @@ __device__ int truncation_rank(const double* sigma, int len, double budget2, int
   return r;
 }
 
+struct SvdWork {
+  double* Xs;    // mx x mx
+  double* vn;    // mx
+  double* sig;   // mx
+  double* sraw;  // mx
+  int* piv;      // mx
+  int* perm;     // mx
+  double* sh;
+  int ldx;
+};
+
+// Singular values and the leading left singular vectors of C = M^T, where
+// M is p x m (ld ldm, destroyed): M Pi = Q R, X = R^T (m x k), Jacobi on
+// X; C = Pi X Q^T so U_C = Pi * normalised columns of X.  Writes U (m x t,
+// ld ldu); returns the truncation rank (all threads).
+__device__ int svd_left(double* M, int ldm, int p, int m, const SvdWork& w, double budget2,
+                        int cap, double* U, int ldu, double* margin_out, int* s_int) {
+  const int k = min(p, m);
+  qrp_inplace(M, ldm, p, m, w.vn, w.piv, w.sh);
+  for (int e = threadIdx.x; e < m * k; e += NT) {
+    const int i = e % m, r = e / m;
+    w.Xs[i + w.ldx * r] = i >= r ? M[r + ldm * i] : 0.0;
+  }
+  __syncthreads();
+  jacobi(w.Xs, w.ldx, m, k, w.vn);
+  for (int q = threadIdx.x; q < k; q += NT) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += w.Xs[i + w.ldx * q] * w.Xs[i + w.ldx * q];
+    w.sraw[q] = sqrt(s);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < k; q += NT) {
+    const double v = w.sraw[q];
+    int rank = 0;
+    for (int o = 0; o < k; ++o) {
+      const double u = w.sraw[o];
+      rank += (u > v) || (u == v && o < q);
+    }
+    w.sig[rank] = v;
+    w.perm[rank] = q;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *s_int = truncation_rank(w.sig, k, budget2, cap, margin_out);
+  __syncthreads();
+  const int t = *s_int;
+  for (int e = threadIdx.x; e < m * t; e += NT) {
+    const int i = e % m, r = e / m;
+    U[w.piv[i] + ldu * r] = w.Xs[i + w.ldx * w.perm[r]] / w.sig[r];
+  }
+  __syncthreads();
+  return t;
+}
+
 // SURVEY.md Appendix A canonical FLOPs of TtTensor::rounded(n; R1,R2 -> t1,t2)
 // (the reference algorithm, not the cheaper one run here).
 __device__ double qr_f(double m, double k) {
@@ -337,48 +452,103 @@ __device__ double round_flops(double n, double R1, double R2, double t1, double 
          n * 2.0 * t1 * q2 * q3 + svd_f(n * t1, q3) + 2.0 * t2 * q3 * n;
 }
 
-__device__ __forceinline__ double mid_val(const TermInfo& t, int n1, int n2, int j, int a,
-                                          int b) {
-  const int jj = t.refl == 2 ? n2 - 1 - j : j;
-  double v = t.base[(long long)n1 * t.r1 + (long long)jj * t.r1 * t.r2 + a + t.r1 * b];
-  if (t.u[1]) v *= t.u[1][j];
-  return v;
+// Stage slice j of every summand's middle core (factor u2[j] and mode-2
+// reflection applied) into Ms with coalesced loads.
+__device__ void stage_slice(double* Ms, const TermInfo* terms, int K, int n1, int n2, int j) {
+  for (int k = 0; k < K; ++k) {
+    const TermInfo& t = terms[k];
+    const int jj = t.refl == 2 ? n2 - 1 - j : j;
+    const double* src = t.base + (long long)n1 * t.r1 + (long long)jj * t.r1 * t.r2;
+    const double f = t.u[1] ? t.u[1][j] : 1.0;
+    const int sz = t.r1 * t.r2;
+    for (int e = threadIdx.x; e < sz; e += NT) Ms[t.ms + e] = f * src[e];
+  }
+}
+
+// X (rows x R2, ld ldxp) = L (rows x R1, ld ldl) blockdiag(Ms_t)
+__device__ void left_times_blockdiag(double* X, int ldxp, const double* L, int ldl, int rows,
+                                     int R2, const double* Ms, const TermInfo* terms,
+                                     const int* colterm) {
+  for (int e = threadIdx.x; e < rows * R2; e += NT) {
+    const int i = e % rows, col = e / rows;
+    const TermInfo& t = terms[colterm[col]];
+    const int b = col - t.off2;
+    const double* mcol = Ms + t.ms + t.r1 * b;
+    const double* lrow = L + i + ldl * t.off1;
+    double s0 = 0.0, s1 = 0.0;
+    int a = 0;
+    for (; a + 1 < t.r1; a += 2) {
+      s0 += lrow[ldl * a] * mcol[a];
+      s1 += lrow[ldl * (a + 1)] * mcol[a + 1];
+    }
+    if (a < t.r1) s0 += lrow[ldl * a] * mcol[a];
+    X[i + ldxp * col] = s0 + s1;
+  }
+}
+
+// out (rows x ncol, ld ldo) with out(r, c) = sum_{b >= c} X(r, b) R3(c, b)
+// (R3 upper trapezoidal, stored in lastT with ld n3): the slice block of
+// the TSQR, written at row offset row0 of B.
+__device__ void times_r3t(double* out, int ldo, const double* X, int ldxp, int rows, int ncol,
+                          int R2, const double* lastT, int n3) {
+  for (int e = threadIdx.x; e < rows * ncol; e += NT) {
+    const int r = e % rows, c = e / rows;
+    double s0 = 0.0, s1 = 0.0;
+    int b = c;
+    for (; b + 1 < R2; b += 2) {
+      s0 += X[r + ldxp * b] * lastT[c + n3 * b];
+      s1 += X[r + ldxp * (b + 1)] * lastT[c + n3 * (b + 1)];
+    }
+    if (b < R2) s0 += X[r + ldxp * b] * lastT[c + n3 * b];
+    out[r + ldo * c] = s0 + s1;
+  }
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT) round_sums_kernel(RoundArgs p) {
+__global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
   extern __shared__ double sm[];
   const int n1 = p.n1, n2 = p.n2, n3 = p.n3;
   const int mx = max(n1, n3);
   const int RM1 = p.RM1, RM2 = p.RM2, HMAX = p.HMAX;
-  // ---- shared-memory carve-up (doubles) ----
-  double* F = sm;                          // n1 x RM1
-  double* lastT = F + n1 * RM1;            // n3 x RM2
+  const int RMX = max(RM1, RM2);
+  const int BROWS = max(HMAX, RM2);
+  // ---- shared-memory carve-up (doubles); see round_smem_bytes ----
+  double* F = sm;                          // n1 x RMX   (cut 2 / output: X2)
+  double* lastT = F + n1 * RMX;            // n3 x RM2
   double* tau = lastT + n3 * RM2;          // mx
   double* Rr = tau + mx;                   // mx x mx
-  double* B = Rr + mx * mx;                // HMAX x mx
-  double* X = B + HMAX * mx;               // n1 x RM2
-  double* P = X + n1 * RM2;                // n1 x RM1
-  double* U1 = P + n1 * RM1;               // n1 x n1
-  double* V2 = U1 + n1 * n1;               // n3 x n3
-  double* sig = V2 + n3 * n3;              // mx
+  double* B = Rr + mx * mx;                // BROWS x mx
+  double* XP = B + BROWS * mx;             // n1 x RMX   (cut 1: X; cut 2: P)
+  double* U1 = XP + n1 * RMX;              // n1 x n1
+  double* Xs = U1 + n1 * n1;               // mx x mx
+  double* Ms = Xs + mx * mx;               // p.MSMAX
+  double* sig = Ms + p.MSMAX;              // mx
   double* sraw = sig + mx;                 // mx
-  double* sh = sraw + mx;                  // 32 scalars
+  double* vn = sraw + mx;                  // mx
+  double* sh = vn + mx;                    // 32 scalars
   int* perm = reinterpret_cast<int*>(sh + 32);          // mx
-  int* colterm = perm + mx;                              // RM2 (col -> term)
-  int* rowterm = colterm + RM2;                          // RM1 (col of F -> term)
+  int* piv = perm + mx;                                  // mx
+  int* colterm = piv + mx;                               // RM2
+  int* rowterm = colterm + RM2;                          // RM1
   TermInfo* terms = reinterpret_cast<TermInfo*>(
-      reinterpret_cast<double*>(rowterm + RM1 + (((RM1 + RM2 + mx) & 1) ? 1 : 0)));
+      reinterpret_cast<double*>(rowterm + RM1 + (((RM1 + RM2) & 1) ? 1 : 0)));
   __shared__ int s_meta[8];
 
   const int o = blockIdx.x;
   if (o >= p.nout) return;
+  long long prof_t = p.prof ? clock64() : 0;
+#define PROF(k)                                                      \
+  if (p.prof && threadIdx.x == 0) {                                  \
+    const long long t_ = clock64();                                  \
+    atomicAdd(&p.prof[k], (unsigned long long)(t_ - prof_t));        \
+    prof_t = t_;                                                     \
+  }
   const long long t0 = p.term_off ? p.term_off[o] : o;
   const int K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
 
   if (threadIdx.x == 0) {
-    int off1 = 0, off2 = 0;
+    int off1 = 0, off2 = 0, ms = 0;
     for (int k = 0; k < K; ++k) {
       const Term tm = p.terms[t0 + k];
       const TSet& s = p.sets[tm.set];
@@ -396,8 +566,10 @@ __global__ void __launch_bounds__(NT) round_sums_kernel(RoundArgs p) {
       ti.u[2] = fac ? fac + n1 + n2 : nullptr;
       ti.off1 = off1;
       ti.off2 = off2;
+      ti.ms = ms;
       off1 += ti.r1;
       off2 += ti.r2;
+      ms += ti.r1 * ti.r2;
       terms[k] = ti;
     }
     s_meta[0] = off1;
@@ -405,7 +577,6 @@ __global__ void __launch_bounds__(NT) round_sums_kernel(RoundArgs p) {
   }
   __syncthreads();
   const int R1 = s_meta[0], R2 = s_meta[1];
-  // column -> term maps
   for (int k = 0; k < K; ++k) {
     const TermInfo& t = terms[k];
     for (int a = threadIdx.x; a < t.r1; a += NT) rowterm[t.off1 + a] = k;
@@ -431,12 +602,11 @@ __global__ void __launch_bounds__(NT) round_sums_kernel(RoundArgs p) {
     }
   }
   __syncthreads();
-
+  PROF(0);
   // ---- 1. QR of last^T ----
   qr_inplace(lastT, n3, n3, R2, tau, sh);
   const int q3 = min(n3, R2);
-  // R3(c, b) = lastT[c + n3*b] for c <= b
-  auto r3 = [&](int c, int b) -> double { return c <= b ? lastT[c + n3 * b] : 0.0; };
+  PROF(1);
 
   // ---- 2. cut 1 TSQR ----
   const bool troute = R1 > n1;
@@ -445,57 +615,66 @@ __global__ void __launch_bounds__(NT) round_sums_kernel(RoundArgs p) {
   const int ns1 = max(1, HMAX / q3);
   for (int j0 = 0; j0 < n2; j0 += ns1) {
     const int jn = min(n2, j0 + ns1);
-    __syncthreads();
     for (int j = j0; j < jn; ++j) {
       const int row0 = (j - j0) * q3;
+      __syncthreads();
+      stage_slice(Ms, terms, K, n1, n2, j);
+      __syncthreads();
       if (troute) {
-        // X = F blockdiag(M_j)  (n1 x R2)
-        for (int e = threadIdx.x; e < n1 * R2; e += NT) {
-          const int i = e % n1, col = e / n1;
-          const TermInfo& t = terms[colterm[col]];
-          const int b = col - t.off2;
-          double s = 0.0;
-          for (int a = 0; a < t.r1; ++a) s += F[i + n1 * (t.off1 + a)] * mid_val(t, n1, n2, j, a, b);
-          X[i + n1 * col] = s;
-        }
+        // T_j^T block: B(row0 + c, i) = sum_b X(i, b) R3(c, b), X = F M_j
+        left_times_blockdiag(XP, n1, F, n1, n1, R2, Ms, terms, colterm);
         __syncthreads();
-        // B(row0 + c, i) = sum_b X(i, b) R3(c, b)
         for (int e = threadIdx.x; e < q3 * n1; e += NT) {
           const int c = e % q3, i = e / q3;
-          double s = 0.0;
-          for (int b = c; b < R2; ++b) s += X[i + n1 * b] * lastT[c + n3 * b];
-          B[row0 + c + HMAX * i] = s;
+          double s0 = 0.0, s1 = 0.0;
+          int b = c;
+          for (; b + 1 < R2; b += 2) {
+            s0 += XP[i + n1 * b] * lastT[c + n3 * b];
+            s1 += XP[i + n1 * (b + 1)] * lastT[c + n3 * (b + 1)];
+          }
+          if (b < R2) s0 += XP[i + n1 * b] * lastT[c + n3 * b];
+          B[row0 + c + HMAX * i] = s0 + s1;
         }
-        __syncthreads();
       } else {
-        // B(row0 + c, off1 + a) = sum_b R3(c, off2 + b) M_tj(a, b)
+        // (M_j R3^T)^T block: B(row0 + c, off1 + a) = sum_b R3(c, off2 + b) M_t(a, b)
         for (int e = threadIdx.x; e < q3 * R1; e += NT) {
           const int c = e % q3, col = e / q3;
           const TermInfo& t = terms[rowterm[col]];
           const int a = col - t.off1;
           double s = 0.0;
-          for (int b = 0; b < t.r2; ++b) s += r3(c, t.off2 + b) * mid_val(t, n1, n2, j, a, b);
+          for (int b = max(0, c - t.off2); b < t.r2; ++b)
+            s += lastT[c + n3 * (t.off2 + b)] * Ms[t.ms + a + t.r1 * b];
           B[row0 + c + HMAX * col] = s;
         }
       }
     }
     __syncthreads();
+    PROF(2);
     qr_update(Rr, mx, B, HMAX, (jn - j0) * q3, c1, sh);
+    PROF(3);
   }
   __syncthreads();
 
-  // ---- 3. C (n1 x c1) into B, norm, Jacobi SVD ----
-  double loc = 0.0;
-  for (int e = threadIdx.x; e < n1 * c1; e += NT) {
-    const int i = e % n1, pp = e / n1;
-    double v;
-    if (troute) {
-      v = pp <= i ? Rr[pp + mx * i] : 0.0;
-    } else {
-      v = 0.0;
-      for (int a = pp; a < R1; ++a) v += F[i + n1 * a] * Rr[pp + mx * a];
+  // ---- 3. SVD of C, through M = C^T (c1 x n1) ----
+  double* Mc;
+  int ldmc;
+  if (troute) {
+    Mc = Rr;  // C^T = R_T
+    ldmc = mx;
+  } else {
+    for (int e = threadIdx.x; e < c1 * n1; e += NT) {  // C^T = R2 F^T
+      const int pp = e % c1, i = e / c1;
+      double v = 0.0;
+      for (int a = pp; a < R1; ++a) v += Rr[pp + mx * a] * F[i + n1 * a];
+      B[pp + HMAX * i] = v;
     }
-    B[i + HMAX * pp] = v;
+    Mc = B;
+    ldmc = HMAX;
+  }
+  __syncthreads();
+  double loc = 0.0;
+  for (int e = threadIdx.x; e < c1 * n1; e += NT) {
+    const double v = Mc[(e % c1) + ldmc * (e / c1)];
     loc += v * v;
   }
   const double norm2 = block_sum(loc, sh + 8);
@@ -513,7 +692,6 @@ __global__ void __launch_bounds__(NT) round_sums_kernel(RoundArgs p) {
       p.out.ranks[2 * o + 1] = 1;
       p.out.off[o] = ok ? (long long)at : -1;
       s_meta[2] = ok ? 1 : 0;
-      s_meta[3] = (int)0;
       reinterpret_cast<long long*>(sh)[20] = (long long)at;
       if (p.margins) {
         p.margins[2 * o] = INFINITY;
@@ -528,68 +706,48 @@ __global__ void __launch_bounds__(NT) round_sums_kernel(RoundArgs p) {
     return;
   }
   const double budget2 = p.eps * p.eps * norm2 / 2.0;
-  jacobi(B, HMAX, n1, c1, nullptr, 0);
-  sorted_norms(B, HMAX, n1, c1, sraw, sig, perm);
-  if (threadIdx.x == 0) {
-    double mg;
-    s_meta[4] = truncation_rank(sig, c1, budget2, p.cap, &mg);
-    if (p.margins) p.margins[2 * o] = mg;
-  }
-  __syncthreads();
-  const int t1 = s_meta[4];
-  // U1(:, r) = C V(:, perm[r]) / sigma_r
-  for (int e = threadIdx.x; e < n1 * t1; e += NT) {
-    const int i = e % n1, r = e / n1;
-    U1[i + n1 * r] = B[i + HMAX * perm[r]] / sig[r];
-  }
-  __syncthreads();
-  // P = U1^T F (t1 x R1)
+  const SvdWork sw{Xs, vn, sig, sraw, piv, perm, sh, mx};
+  PROF(4);
+  double mg1 = 0.0;
+  const int t1 = svd_left(Mc, ldmc, c1, n1, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
+  if (p.margins && threadIdx.x == 0) p.margins[2 * o] = mg1;
+  PROF(5);
+  // P = U1^T F (t1 x R1) into XP (ld n1)
   for (int e = threadIdx.x; e < t1 * R1; e += NT) {
     const int r = e % t1, col = e / t1;
     double s = 0.0;
     for (int i = 0; i < n1; ++i) s += U1[i + n1 * r] * F[i + n1 * col];
-    P[r + n1 * col] = s;
+    XP[r + n1 * col] = s;
   }
 
   // ---- 4. cut 2 TSQR over S_j = P blockdiag(M_j) R3^T (t1 x q3) ----
   for (int e = threadIdx.x; e < mx * mx; e += NT) Rr[e] = 0.0;
+  double* X2 = F;  // F is dead once P exists
   const int ns2 = max(1, HMAX / t1);
   for (int j0 = 0; j0 < n2; j0 += ns2) {
     const int jn = min(n2, j0 + ns2);
-    __syncthreads();
     for (int j = j0; j < jn; ++j) {
       const int row0 = (j - j0) * t1;
-      for (int e = threadIdx.x; e < t1 * R2; e += NT) {
-        const int r = e % t1, col = e / t1;
-        const TermInfo& t = terms[colterm[col]];
-        const int b = col - t.off2;
-        double s = 0.0;
-        for (int a = 0; a < t.r1; ++a) s += P[r + n1 * (t.off1 + a)] * mid_val(t, n1, n2, j, a, b);
-        X[r + n1 * col] = s;
-      }
       __syncthreads();
-      for (int e = threadIdx.x; e < t1 * q3; e += NT) {
-        const int r = e % t1, c = e / t1;
-        double s = 0.0;
-        for (int b = c; b < R2; ++b) s += X[r + n1 * b] * lastT[c + n3 * b];
-        B[row0 + r + HMAX * c] = s;
-      }
+      stage_slice(Ms, terms, K, n1, n2, j);
       __syncthreads();
+      left_times_blockdiag(X2, n1, XP, n1, t1, R2, Ms, terms, colterm);
+      __syncthreads();
+      times_r3t(B + row0, HMAX, X2, n1, t1, q3, R2, lastT, n3);
     }
+    __syncthreads();
+    PROF(6);
     qr_update(Rr, mx, B, HMAX, (jn - j0) * t1, q3, sh);
+    PROF(7);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < q3 * q3; e += NT) {
-    const int i = e % q3, c = e / q3;
-    V2[i + n3 * c] = i == c ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  jacobi(Rr, mx, q3, q3, V2, n3);
-  sorted_norms(Rr, mx, q3, q3, sraw, sig, perm);
+  PROF(8);
+  // ---- SVD through M = R_S (q3 x q3): left vectors of R_S^T = V2 -> B ----
+  double mg2 = 0.0;
+  const int t2 = svd_left(Rr, mx, q3, q3, sw, budget2, p.cap, B, HMAX, &mg2, &s_meta[5]);
+  PROF(9);
   if (threadIdx.x == 0) {
-    double mg;
-    const int t2 = truncation_rank(sig, q3, budget2, p.cap, &mg);
-    if (p.margins) p.margins[2 * o + 1] = mg;
+    if (p.margins) p.margins[2 * o + 1] = mg2;
     const long long sz = (long long)n1 * t1 + (long long)n2 * t1 * t2 + (long long)t2 * n3;
     const unsigned long long at = atomicAdd(p.out.used, (unsigned long long)sz);
     const bool ok = (long long)(at + sz) <= p.out.capacity;
@@ -608,61 +766,40 @@ __global__ void __launch_bounds__(NT) round_sums_kernel(RoundArgs p) {
       atomicAdd(&p.acc[1], 8.0 * (in_sz + (double)sz));
     }
     s_meta[2] = ok ? 1 : 0;
-    s_meta[5] = t2;
     reinterpret_cast<long long*>(sh)[20] = (long long)at;
   }
   __syncthreads();
   if (!s_meta[2]) return;
-  const int t2 = s_meta[5];
   double* dst = p.out.base + reinterpret_cast<long long*>(sh)[20];
   double* dmid = dst + (long long)n1 * t1;
   double* dlast = dmid + (long long)n2 * t1 * t2;
   // ---- 5. outputs ----
   for (int e = threadIdx.x; e < n1 * t1; e += NT) dst[e] = U1[e];
-  // W2 = V2(:, perm[:t2]) (q3 x t2) kept in the tail of sraw/sig? use B rows
-  // beyond the S_j block: store W2 in Rr (free now).
-  for (int e = threadIdx.x; e < q3 * t2; e += NT) {
-    const int c = e % q3, s = e / q3;
-    Rr[c + mx * s] = V2[c + n3 * perm[s]];
-  }
-  __syncthreads();
-  for (int j = 0; j < n2; ++j) {
-    for (int e = threadIdx.x; e < t1 * R2; e += NT) {
-      const int r = e % t1, col = e / t1;
-      const TermInfo& t = terms[colterm[col]];
-      const int b = col - t.off2;
-      double s = 0.0;
-      for (int a = 0; a < t.r1; ++a) s += P[r + n1 * (t.off1 + a)] * mid_val(t, n1, n2, j, a, b);
-      X[r + n1 * col] = s;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < t1 * q3; e += NT) {
-      const int r = e % t1, c = e / t1;
-      double s = 0.0;
-      for (int b = c; b < R2; ++b) s += X[r + n1 * b] * lastT[c + n3 * b];
-      B[r + HMAX * c] = s;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < t1 * t2; e += NT) {
-      const int r = e % t1, s = e / t1;
-      double acc = 0.0;
-      for (int c = 0; c < q3; ++c) acc += B[r + HMAX * c] * Rr[c + mx * s];
-      dmid[(long long)j * t1 * t2 + r + t1 * s] = acc;
-    }
-    __syncthreads();
-  }
-  // last = (Q3 [W2; 0])^T : G (n3 x t2) in B
+  // W2 = V2 (q3 x t2) from B into Rr (ld mx); G = [W2; 0] into Xs (ld mx)
   for (int e = threadIdx.x; e < n3 * t2; e += NT) {
     const int c = e % n3, s = e / n3;
-    B[c + HMAX * s] = c < q3 ? Rr[c + mx * s] : 0.0;
+    const double v = c < q3 ? B[c + HMAX * s] : 0.0;
+    Xs[c + mx * s] = v;
+    if (c < q3) Rr[c + mx * s] = v;
   }
   __syncthreads();
+  // Z = R3^T W2 (R2 x t2, ld BROWS) into B
+  double* Z = B;
+  for (int e = threadIdx.x; e < R2 * t2; e += NT) {
+    const int b = e % R2, s = e / R2;
+    double acc = 0.0;
+    const int cm = min(b, q3 - 1);
+    for (int c = 0; c <= cm; ++c) acc += lastT[c + n3 * b] * Rr[c + mx * s];
+    Z[b + BROWS * s] = acc;
+  }
+  // last = (Q3 G)^T, Q3 = H_0 ... H_{q3-1}
   const int kmax = min(n3, R2);
   for (int k = kmax - 1; k >= 0; --k) {
     const double t = tau[k];
+    __syncthreads();
     if (t != 0.0) {
       for (int s = threadIdx.x; s < t2; s += NT) {
-        double* g = B + HMAX * s;
+        double* g = Xs + mx * s;
         double w = g[k];
         for (int i = k + 1; i < n3; ++i) w += lastT[i + n3 * k] * g[i];
         w *= t;
@@ -670,29 +807,80 @@ __global__ void __launch_bounds__(NT) round_sums_kernel(RoundArgs p) {
         for (int i = k + 1; i < n3; ++i) g[i] -= w * lastT[i + n3 * k];
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int e = threadIdx.x; e < t2 * n3; e += NT) {
     const int s = e % t2, kk = e / t2;
-    dlast[s + t2 * kk] = B[kk + HMAX * s];
+    dlast[s + t2 * kk] = Xs[kk + mx * s];
   }
+  // middle_j = (P blockdiag(M_j)) Z
+  for (int j = 0; j < n2; ++j) {
+    __syncthreads();
+    stage_slice(Ms, terms, K, n1, n2, j);
+    __syncthreads();
+    left_times_blockdiag(X2, n1, XP, n1, t1, R2, Ms, terms, colterm);
+    __syncthreads();
+    for (int e = threadIdx.x; e < t1 * t2; e += NT) {
+      const int r = e % t1, s = e / t1;
+      double a0 = 0.0, a1 = 0.0;
+      int b = 0;
+      for (; b + 1 < R2; b += 2) {
+        a0 += X2[r + n1 * b] * Z[b + BROWS * s];
+        a1 += X2[r + n1 * (b + 1)] * Z[b + 1 + BROWS * s];
+      }
+      if (b < R2) a0 += X2[r + n1 * b] * Z[b + BROWS * s];
+      dmid[(long long)j * t1 * t2 + r + t1 * s] = a0 + a1;
+    }
+  }
+  __syncthreads();
+  PROF(10);
+#undef PROF
 }
 
 // Shared-memory bytes of the plan above.
-size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX) {
+size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int MSMAX) {
   (void)n2;
   const size_t mx = n1 > n3 ? n1 : n3;
-  size_t d = (size_t)n1 * RM1 + (size_t)n3 * RM2 + mx + mx * mx + (size_t)HMAX * mx +
-             (size_t)n1 * RM2 + (size_t)n1 * RM1 + (size_t)n1 * n1 + (size_t)n3 * n3 + 2 * mx +
-             32;
-  size_t ints = mx + RM2 + RM1 + 1;
+  const size_t RMX = RM1 > RM2 ? RM1 : RM2;
+  const size_t BROWS = HMAX > RM2 ? HMAX : RM2;
+  size_t d = (size_t)n1 * RMX + (size_t)n3 * RM2 + mx + mx * mx + BROWS * mx +
+             (size_t)n1 * RMX + (size_t)n1 * n1 + mx * mx + (size_t)MSMAX + 3 * mx + 32;
+  size_t ints = 2 * mx + RM2 + RM1 + 1;
   size_t bytes = d * 8 + ((ints * 4 + 7) / 8) * 8 + sizeof(TermInfo) * kMaxTerms + 64;
   return bytes;
 }
 
+// Per-launch bounds: max over outputs of summed ranks, middle sizes, terms.
+__global__ void round_bounds_kernel(RoundArgs p, int* bounds) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < p.nout; o += gridDim.x * blockDim.x) {
+    const long long t0 = p.term_off ? p.term_off[o] : o;
+    const int K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
+    int r1 = 0, r2 = 0, ms = 0;
+    for (int k = 0; k < K; ++k) {
+      const Term tm = p.terms[t0 + k];
+      const TSet& s = p.sets[tm.set];
+      const int a = s.ranks[2 * tm.idx], b = s.ranks[2 * tm.idx + 1];
+      r1 += a;
+      r2 += b;
+      ms += a * b;
+    }
+    atomicMax(&bounds[0], r1);
+    atomicMax(&bounds[1], r2);
+    atomicMax(&bounds[2], ms);
+    atomicMax(&bounds[3], K);
+  }
+}
+
+cudaError_t launch_round_bounds(const RoundArgs& a, int* bounds, cudaStream_t st) {
+  if (a.nout == 0) return cudaSuccess;
+  const int blocks = min(1184, (a.nout + 255) / 256);
+  round_bounds_kernel<<<blocks, 256, 0, st>>>(a, bounds);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_round(const RoundArgs& a, cudaStream_t st) {
   if (a.nout == 0) return cudaSuccess;
-  const size_t smem = round_smem_bytes(a.n1, a.n2, a.n3, a.RM1, a.RM2, a.HMAX);
+  const size_t smem = round_smem_bytes(a.n1, a.n2, a.n3, a.RM1, a.RM2, a.HMAX, a.MSMAX);
   cudaError_t e = cudaFuncSetAttribute(round_sums_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -8,7 +8,7 @@ namespace ttdvm {
 
 constexpr int kMaxSets = 8;
 constexpr int kMaxTerms = 16;     // summands per rounded output
-constexpr int kRoundThreads = 256;
+constexpr int kRoundThreads = 128;
 
 // A set of packed TT tensors (ttdvm_tt_batch layout) resident in an arena.
 struct TSet {
@@ -63,9 +63,11 @@ struct RoundArgs {
   int* status;                  // [kStWords]
   double* margins;              // optional [2*nout]
   double* acc;                  // [2]: canonical FLOPs, compulsory bytes (atomicAdd)
+  unsigned long long* prof;     // optional [16] per-phase SM cycles (diagnostics)
   // shared-memory plan (doubles), chosen by the host launcher
   int RM1, RM2;                 // bounds on the summed input ranks
   int HMAX;                     // rows of the TSQR block buffer
+  int MSMAX;                    // doubles of the staged middle slices
 };
 
 }  // namespace ttdvm

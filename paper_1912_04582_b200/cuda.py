@@ -31,7 +31,7 @@ EXPORTS = (
     "ttdvm_cuda_round_batch", "ttdvm_cuda_result_layout", "ttdvm_cuda_result_download",
     "ttdvm_cuda_macro_batch", "ttdvm_cuda_collision_batch", "ttdvm_cuda_phase_times",
     "ttdvm_cuda_launch_count", "ttdvm_cuda_set_profiling", "ttdvm_cuda_phase_work",
-    "ttdvm_cuda_timed_step", "ttdvm_cuda_fp64_peak",
+    "ttdvm_cuda_timed_step", "ttdvm_cuda_fp64_peak", "ttdvm_cuda_round_profile",
 )
 
 OK, EINVAL, EDOMAIN, ENOMEM, ECUDA, ENCCL = range(6)
@@ -88,6 +88,7 @@ def load_library(path: str = LIB_PATH):
         "ttdvm_cuda_phase_work": (C.c_int, [vp, vp, vp, vp]),
         "ttdvm_cuda_timed_step": (C.c_int, [vp, dbl, dbl, i32, i32, vp]),
         "ttdvm_cuda_fp64_peak": (C.c_int, [vp, vp]),
+        "ttdvm_cuda_round_profile": (C.c_int, [vp, C.c_int, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -272,6 +273,12 @@ class Context:
         t = np.zeros(1)
         self._check(self.lib.ttdvm_cuda_fp64_peak(self.h, _ptr(t)))
         return float(t[0])
+
+    def round_profile(self, on: bool = True) -> np.ndarray:
+        """Per-phase cycles of the rounding kernel since the last call."""
+        out = np.zeros(16, dtype=np.uint64)
+        self._check(self.lib.ttdvm_cuda_round_profile(self.h, 1 if on else 0, _ptr(out)))
+        return out
 
     def launch_count(self) -> int:
         return int(self.lib.ttdvm_cuda_launch_count(self.h))
