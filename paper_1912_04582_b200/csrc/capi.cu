@@ -315,12 +315,14 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   const int mx = n;
   // TSQR block height: as tall as the shared-memory budget allows, aiming
   // at >= 3 resident CTAs per SM
-  int HMAX = std::max(mx, std::min(4 * mx, 128));
-  size_t smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX, MSMAX);
-  while (smem > 75 * 1024 && HMAX > mx) {
-    HMAX = std::max(mx, HMAX - mx);
-    smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX, MSMAX);
-  }
+  // TSQR block height: n <= 32 runs the SMALL kernel (one slice per update,
+  // h <= 32, few registers, more resident CTAs); larger grids hold <= 48
+  // rows per update
+  if (mx > 48)
+    throw Fail{TTDVM_EINVAL, "velocity grids above 48 nodes per axis need the 256-thread "
+                             "rounding variant (not built yet)"};
+  const int HMAX = mx <= 32 ? mx : 48;
+  const size_t smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX, MSMAX);
   if (smem > 227 * 1024)
     throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory (n=" + std::to_string(n) +
                                  ", summed ranks " + std::to_string(RM1) + "x" +

@@ -70,7 +70,35 @@ __device__ double block_sum(double v, double* red) {
   return s;
 }
 
-// LAPACK dlarfg on (alpha, ||x||^2): H = I - tau v v^T, v = [1; x*scale].
+// FP64 reciprocal and reciprocal square root with an FP32 seed and two
+// Newton steps in FP64 (23 -> 46 -> 92 bits, i.e. correct to a few ulps):
+// the IEEE-exact double div/sqrt sequences sit on the serial critical path
+// of every Householder and Jacobi step.  Exponents are split off exactly so
+// the FP32 seed never over- or underflows.
+__device__ __forceinline__ double fast_rcp(double x) {
+  const long long bits = __double_as_longlong(x);
+  const int e = (int)((bits >> 52) & 0x7ff) - 1023;
+  const double m = __longlong_as_double((bits & ~(0x7ffLL << 52)) | (1023LL << 52));  // [1,2)
+  double r = (double)__frcp_rn((float)m);
+  r = r * (2.0 - m * r);
+  r = r * (2.0 - m * r);
+  return r * __longlong_as_double((long long)(1023 - e) << 52);
+}
+
+__device__ __forceinline__ double fast_rsqrt(double x) {  // x > 0, normal
+  const long long bits = __double_as_longlong(x);
+  int e = (int)((bits >> 52) & 0x7ff) - 1023;
+  const int odd = e & 1;
+  e -= odd;  // even exponent: x = m * 2^e, m in [1, 4)
+  const double m = __longlong_as_double((bits & ~(0x7ffLL << 52)) | ((long long)(1023 + odd) << 52));
+  double r = (double)rsqrtf((float)m);
+  r = r * (1.5 - 0.5 * m * r * r);
+  r = r * (1.5 - 0.5 * m * r * r);
+  return r * __longlong_as_double((long long)(1023 - e / 2) << 52);
+}
+
+// LAPACK dlarfg on (alpha, ||x||^2): H = I - tau v v^T, v = [1; x*scale],
+// tau = (beta - alpha)/beta = 1 - alpha/beta, with 1/|beta| from one rsqrt.
 __device__ __forceinline__ void larfg(double alpha, double sigma2, double& beta, double& tau,
                                       double& scale) {
   if (sigma2 == 0.0) {
@@ -79,10 +107,31 @@ __device__ __forceinline__ void larfg(double alpha, double sigma2, double& beta,
     scale = 0.0;
     return;
   }
-  const double nrm = sqrt(alpha * alpha + sigma2);
+  const double h = alpha * alpha + sigma2;
+  const double ri = fast_rsqrt(h);
+  const double nrm = h * ri;
   beta = alpha >= 0.0 ? -nrm : nrm;
-  tau = (beta - alpha) / beta;
-  scale = 1.0 / (alpha - beta);
+  const double rb = alpha >= 0.0 ? -ri : ri;  // 1 / beta
+  tau = 1.0 - alpha * rb;
+  scale = fast_rcp(alpha - beta);
+}
+
+// Visit (r, c) in [0, rows) x [0, cols) without integer division: threads
+// are split into power-of-two row lanes (r = tid & (rp - 1)) and column
+// strides.  No barriers or shuffles may be used inside f.
+template <class Fn>
+__device__ __forceinline__ void for2d(int rows, int cols, Fn&& f) {
+  if (rows <= 0 || cols <= 0) return;
+  const int lg = rows <= 1 ? 0 : 32 - __clz(rows - 1);
+  if ((1 << lg) <= NT) {
+    const int r = threadIdx.x & ((1 << lg) - 1);
+    if (r >= rows) return;
+    const int step = NT >> lg;
+    for (int c = threadIdx.x >> lg; c < cols; c += step) f(r, c);
+  } else {
+    for (int r = threadIdx.x; r < rows; r += NT)
+      for (int c = 0; c < cols; ++c) f(r, c);
+  }
 }
 
 __device__ __forceinline__ int floor_pow2(int x) {
@@ -133,65 +182,87 @@ __device__ void qr_inplace(double* A, int lda, int m, int ncols, double* tau, do
   }
 }
 
-// QR of [R; B] -> R, R upper c x c (ld ldr), B h x c (ld ldb); B destroyed.
-// Threads: groups of TPC lanes per column, rows strided inside the group.
-template <int TPC>
-__device__ void qr_update_t(double* R, int ldr, double* B, int ldb, int h, int c, double* sh) {
+// QR of [R; B] -> R, R upper c x c (ld ldr), B h x c (ld ldb) read once.
+// Groups of TPC threads own one column each (c <= NT / TPC) and keep its
+// rows (sub, sub + TPC, ...) in registers; the Householder vector of step k
+// is broadcast through vbuf (double-buffered), so each column step costs one
+// __syncthreads.  The owner of column k + 1 learns its squared norm while
+// applying step k.
+template <int TPC, int NR>
+__device__ void qr_update_reg(double* R, int ldr, const double* B, int ldb, int h, int c,
+                              double* vbuf, int vld, double* sh) {
   const int g = threadIdx.x / TPC, sub = threadIdx.x % TPC;
-  const int ngroups = NT / TPC;
-  if (threadIdx.x < 32) {  // sigma2 of column 0 (all of warp 0 reaches the shuffles)
-    double s = 0.0;
-    if (g == 0)
-      for (int i = sub; i < h; i += TPC) s += B[i] * B[i];
-    s = group_sum<TPC>(s);
-    if (g == 0 && sub == 0) sh[0] = s;
+  double x[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    const int row = sub + TPC * q;
+    x[q] = (g < c && row < h) ? B[row + ldb * g] : 0.0;
+  }
+  double s2 = 0.0;  // squared norm of the own column (valid in the owner of k)
+#pragma unroll
+  for (int q = 0; q < NR; ++q) s2 += x[q] * x[q];
+  s2 = group_sum<TPC>(s2);
+  __syncthreads();  // B may be overwritten by the caller only after all loads
+  for (int k = 0; k < c; ++k) {
+    double* v = vbuf + (k & 1) * vld;
+    if (g == k) {
+      double beta, t, sc;
+      larfg(R[k + ldr * k], s2, beta, t, sc);
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const int row = sub + TPC * q;
+        x[q] *= sc;
+        if (row < h) v[row] = x[q];
+      }
+      if (sub == 0) {
+        sh[(k & 1)] = t;
+        if (t != 0.0) R[k + ldr * k] = beta;
+      }
+    }
+    __syncthreads();
+    const double t = sh[k & 1];
+    const bool act = g > k && g < c;
+    double w = 0.0, rkl = 0.0;
+    if (act && t != 0.0) {
+      rkl = R[k + ldr * g];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const int row = sub + TPC * q;
+        if (row < h) w += v[row] * x[q];
+      }
+    }
+    w = group_sum<TPC>(w);
+    double ss = 0.0;
+    if (act && t != 0.0) {
+      w = t * (w + rkl);
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const int row = sub + TPC * q;
+        if (row < h) x[q] -= w * v[row];
+      }
+      if (sub == 0) R[k + ldr * g] = rkl - w;
+    }
+    if (g == k + 1) {  // next pivot column: its squared norm for step k + 1
+#pragma unroll
+      for (int q = 0; q < NR; ++q) ss += x[q] * x[q];
+    }
+    ss = group_sum<TPC>(ss);
+    if (g == k + 1) s2 = ss;
   }
   __syncthreads();
-  for (int k = 0; k < c; ++k) {
-    double beta, t, sc;
-    larfg(R[k + ldr * k], sh[k & 1], beta, t, sc);
-    if (t != 0.0) {
-      for (int i = threadIdx.x; i < h; i += NT) B[i + ldb * k] *= sc;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && t != 0.0) R[k + ldr * k] = beta;
-    const double* v = B + ldb * k;
-    for (int base = k + 1; base < c; base += ngroups) {  // uniform trip count
-      const int l = base + g;
-      const bool act = l < c;
-      double* col = B + ldb * (act ? l : k);
-      double w = 0.0;
-      if (t != 0.0) {
-        if (act)
-          for (int i = sub; i < h; i += TPC) w += v[i] * col[i];
-        w = group_sum<TPC>(w);
-        if (act) w = t * (w + R[k + ldr * l]);
-      }
-      double s = 0.0;
-      if (act) {
-        for (int i = sub; i < h; i += TPC) {
-          const double x = col[i] - w * v[i];
-          col[i] = x;
-          s += x * x;
-        }
-        if (sub == 0) R[k + ldr * l] -= w;
-      }
-      s = group_sum<TPC>(s);
-      if (act && l == k + 1 && sub == 0) sh[(k + 1) & 1] = s;
-    }
-    __syncthreads();
-  }
 }
 
-__device__ void qr_update(double* R, int ldr, double* B, int ldb, int h, int c, double* sh) {
-  const int tpc = min(32, floor_pow2(max(1, NT / max(c, 1))));
-  switch (tpc) {
-    case 32: qr_update_t<32>(R, ldr, B, ldb, h, c, sh); break;
-    case 16: qr_update_t<16>(R, ldr, B, ldb, h, c, sh); break;
-    case 8: qr_update_t<8>(R, ldr, B, ldb, h, c, sh); break;
-    case 4: qr_update_t<4>(R, ldr, B, ldb, h, c, sh); break;
-    case 2: qr_update_t<2>(R, ldr, B, ldb, h, c, sh); break;
-    default: qr_update_t<1>(R, ldr, B, ldb, h, c, sh); break;
+// SMALL variant (n <= 32): one slice per update, h <= 32 rows, 8 per thread;
+// large variant (n <= 48): h <= 48, 24 rows per thread.
+template <bool SMALL>
+__device__ void qr_update(double* R, int ldr, const double* B, int ldb, int h, int c,
+                          double* vbuf, int vld, double* sh) {
+  if (SMALL) {
+    qr_update_reg<4, 8>(R, ldr, B, ldb, h, c, vbuf, vld, sh);  // c <= 32, h <= 32
+  } else if (c <= NT / 4) {
+    qr_update_reg<4, 12>(R, ldr, B, ldb, h, c, vbuf, vld, sh);  // h <= 48
+  } else {
+    qr_update_reg<2, 24>(R, ldr, B, ldb, h, c, vbuf, vld, sh);  // h <= 48, c <= 64
   }
 }
 
@@ -289,11 +360,11 @@ __device__ void qrp_inplace(double* M, int ldm, int p, int m, double* vn, int* p
 // tracked squared column norms (one dot product per pair and round; the
 // norms are refreshed at every sweep).
 template <int TPP>
-__device__ void jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
+__device__ int jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
   const int cp = c + (c & 1);
   const int npairs = cp / 2;
   const int pi = threadIdx.x / TPP, sub = threadIdx.x % TPP;
-  const double tol = 1e-15;
+  const double tol2 = 1e-30;  // (1e-15)^2, |gamma| > 1e-15 sqrt(alpha beta)
   for (int sweep = 0; sweep < 60; ++sweep) {
     for (int j = threadIdx.x; j < c; j += NT) {
       double s = 0.0;
@@ -302,11 +373,18 @@ __device__ void jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
     }
     __syncthreads();
     bool rotated = false;
+    bool big = false;  // some rotation in this sweep had |gamma| > 1e-9 sqrt(alpha beta)
     for (int r = 0; r < cp - 1; ++r) {
       for (int base = 0; base < npairs; base += NT / TPP) {
         const int pp = base + pi;
-        const int a = pp == 0 ? 0 : ((pp + r - 1) % (cp - 1)) + 1;
-        const int b = ((cp - 1 - pp + r - 1) % (cp - 1)) + 1;
+        // round-robin pairs: a = (pp + r - 1) mod (cp - 1) + 1 (pp > 0),
+        // b = (cp - 2 - pp + r) mod (cp - 1) + 1; both arguments < 2 (cp - 1)
+        int a = pp + r - 1;
+        if (a >= cp - 1) a -= cp - 1;
+        a = pp == 0 ? 0 : a + 1;
+        int b = cp - 2 - pp + r;
+        if (b >= cp - 1) b -= cp - 1;
+        b += 1;
         const bool live = pp < npairs && a < c && b < c;
         double ga = 0.0;
         double* x = X + ldx * (live ? a : 0);
@@ -316,44 +394,57 @@ __device__ void jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
         ga = group_sum<TPP>(ga);
         if (live && ga != 0.0) {
           const double al = nrm[a], be = nrm[b];
-          if (fabs(ga) > tol * sqrt(al) * sqrt(be)) {
-            rotated = true;
-            const double zeta = (be - al) / (2.0 * ga);
-            double t;
-            if (fabs(zeta) > 1e150) {
-              t = 0.5 / zeta;
-            } else {
-              t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            }
-            const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          if (ga * ga > tol2 * al * be) {
+            big = big || (ga * ga > 1e-18 * al * be);
+            // t = sign(d) 2 ga / (|d| + sqrt(d^2 + 4 ga^2)), d = be - al: the
+            // angle needs no more than FP32 accuracy (an inexact angle only
+            // slows convergence); cs, sn are normalised in FP64 so the
+            // rotation stays orthogonal to working precision.
+            const double d = be - al;
+            const double mag = fmax(fabs(d), 2.0 * fabs(ga));
+            const int ex = (int)((__double_as_longlong(mag) >> 52) & 0x7ff) - 1023;
+            const double sc = __longlong_as_double((long long)(1023 - ex) << 52);
+            const float df = (float)(d * sc), gf = (float)(ga * sc);
+            const float tf = copysignf(1.0f, df) * (2.0f * gf) /
+                             (fabsf(df) + sqrtf(df * df + 4.0f * gf * gf));
+            const double t = (double)tf;
+            rotated = rotated || (tf != 0.0f);  // an FP32-underflowed angle is converged
+            const double cs = fast_rsqrt(1.0 + t * t), sn = cs * t;
             for (int i = sub; i < m; i += TPP) {
               const double xi = x[i], yi = y[i];
               x[i] = cs * xi - sn * yi;
               y[i] = sn * xi + cs * yi;
             }
             if (sub == 0) {
-              nrm[a] = al - t * ga;
-              nrm[b] = be + t * ga;
+              const double c2 = cs * cs, tg = 2.0 * t * ga, t2 = t * t;
+              nrm[a] = c2 * (al - tg + t2 * be);
+              nrm[b] = c2 * (be + tg + t2 * al);
             }
           }
         }
       }
       __syncthreads();
     }
-    if (!__syncthreads_or(rotated ? 1 : 0)) break;
+    // rotations in this sweep were all below 1e-9 of the column norms: by
+    // the quadratic convergence of cyclic Jacobi the remaining couplings
+    // are O(1e-18), below the 1e-15 threshold -- no verification sweep
+    const int any_rot = __syncthreads_or(rotated ? 1 : 0);
+    const int any_big = __syncthreads_or(big ? 1 : 0);
+    if (!any_rot || !any_big) return sweep + 1;
   }
+  return 60;
 }
 
-__device__ void jacobi(double* X, int ldx, int m, int c, double* nrm) {
+__device__ int jacobi(double* X, int ldx, int m, int c, double* nrm) {
   const int npairs = (c + 1) / 2;
   const int tpp = min(32, floor_pow2(max(1, NT / max(npairs, 1))));
   switch (tpp) {
-    case 32: jacobi_t<32>(X, ldx, m, c, nrm); break;
-    case 16: jacobi_t<16>(X, ldx, m, c, nrm); break;
-    case 8: jacobi_t<8>(X, ldx, m, c, nrm); break;
-    case 4: jacobi_t<4>(X, ldx, m, c, nrm); break;
-    case 2: jacobi_t<2>(X, ldx, m, c, nrm); break;
-    default: jacobi_t<1>(X, ldx, m, c, nrm); break;
+    case 32: return jacobi_t<32>(X, ldx, m, c, nrm);
+    case 16: return jacobi_t<16>(X, ldx, m, c, nrm);
+    case 8: return jacobi_t<8>(X, ldx, m, c, nrm);
+    case 4: return jacobi_t<4>(X, ldx, m, c, nrm);
+    case 2: return jacobi_t<2>(X, ldx, m, c, nrm);
+    default: return jacobi_t<1>(X, ldx, m, c, nrm);
   }
 }
 
@@ -379,6 +470,7 @@ __device__ int truncation_rank(const double* sigma, int len, double budget2, int
 }
 
 struct SvdWork {
+  unsigned long long* prof;  // optional sweep counter
   double* Xs;    // mx x mx
   double* vn;    // mx
   double* sig;   // mx
@@ -397,12 +489,14 @@ __device__ int svd_left(double* M, int ldm, int p, int m, const SvdWork& w, doub
                         int cap, double* U, int ldu, double* margin_out, int* s_int) {
   const int k = min(p, m);
   qrp_inplace(M, ldm, p, m, w.vn, w.piv, w.sh);
-  for (int e = threadIdx.x; e < m * k; e += NT) {
-    const int i = e % m, r = e / m;
-    w.Xs[i + w.ldx * r] = i >= r ? M[r + ldm * i] : 0.0;
-  }
+  for2d(m, k, [&](int i, int r) { w.Xs[i + w.ldx * r] = i >= r ? M[r + ldm * i] : 0.0; });
   __syncthreads();
-  jacobi(w.Xs, w.ldx, m, k, w.vn);
+  const int sweeps = jacobi(w.Xs, w.ldx, m, k, w.vn);
+  if (w.prof && threadIdx.x == 0) {
+    atomicAdd(&w.prof[12], (unsigned long long)sweeps);
+    atomicAdd(&w.prof[13], 1ULL);
+    if (sweeps >= 60) atomicAdd(&w.prof[14], 1ULL);
+  }
   for (int q = threadIdx.x; q < k; q += NT) {
     double s = 0.0;
     for (int i = 0; i < m; ++i) s += w.Xs[i + w.ldx * q] * w.Xs[i + w.ldx * q];
@@ -423,10 +517,9 @@ __device__ int svd_left(double* M, int ldm, int p, int m, const SvdWork& w, doub
   if (threadIdx.x == 0) *s_int = truncation_rank(w.sig, k, budget2, cap, margin_out);
   __syncthreads();
   const int t = *s_int;
-  for (int e = threadIdx.x; e < m * t; e += NT) {
-    const int i = e % m, r = e / m;
+  for2d(m, t, [&](int i, int r) {
     U[w.piv[i] + ldu * r] = w.Xs[i + w.ldx * w.perm[r]] / w.sig[r];
-  }
+  });
   __syncthreads();
   return t;
 }
@@ -465,48 +558,89 @@ __device__ void stage_slice(double* Ms, const TermInfo* terms, int K, int n1, in
   }
 }
 
-// X (rows x R2, ld ldxp) = L (rows x R1, ld ldl) blockdiag(Ms_t)
+// X (rows x R2, ld ldxp) = L (rows x R1, ld ldl) blockdiag(Ms_t); each
+// thread computes a 4-row strip of one column (4 independent FMA chains,
+// one broadcast Ms load per 4 FMAs).
 __device__ void left_times_blockdiag(double* X, int ldxp, const double* L, int ldl, int rows,
                                      int R2, const double* Ms, const TermInfo* terms,
                                      const int* colterm) {
-  for (int e = threadIdx.x; e < rows * R2; e += NT) {
-    const int i = e % rows, col = e / rows;
+  const int ngr = (rows + 3) >> 2;
+  for2d(ngr, R2, [&](int ig, int col) {
+    const int i0 = ig << 2;
     const TermInfo& t = terms[colterm[col]];
     const int b = col - t.off2;
     const double* mcol = Ms + t.ms + t.r1 * b;
-    const double* lrow = L + i + ldl * t.off1;
-    double s0 = 0.0, s1 = 0.0;
-    int a = 0;
-    for (; a + 1 < t.r1; a += 2) {
-      s0 += lrow[ldl * a] * mcol[a];
-      s1 += lrow[ldl * (a + 1)] * mcol[a + 1];
+    const double* lr = L + ldl * t.off1;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (i0 + 3 < rows) {
+      for (int a = 0; a < t.r1; ++a) {
+        const double m = mcol[a];
+        const double* l = lr + ldl * a + i0;
+        a0 += l[0] * m;
+        a1 += l[1] * m;
+        a2 += l[2] * m;
+        a3 += l[3] * m;
+      }
+      double* xo = X + i0 + ldxp * col;
+      xo[0] = a0;
+      xo[1] = a1;
+      xo[2] = a2;
+      xo[3] = a3;
+    } else {
+      for (int a = 0; a < t.r1; ++a) {
+        const double m = mcol[a];
+        const double* l = lr + ldl * a;
+        a0 += l[i0] * m;
+        if (i0 + 1 < rows) a1 += l[i0 + 1] * m;
+        if (i0 + 2 < rows) a2 += l[i0 + 2] * m;
+      }
+      X[i0 + ldxp * col] = a0;
+      if (i0 + 1 < rows) X[i0 + 1 + ldxp * col] = a1;
+      if (i0 + 2 < rows) X[i0 + 2 + ldxp * col] = a2;
     }
-    if (a < t.r1) s0 += lrow[ldl * a] * mcol[a];
-    X[i + ldxp * col] = s0 + s1;
-  }
+  });
 }
 
-// out (rows x ncol, ld ldo) with out(r, c) = sum_{b >= c} X(r, b) R3(c, b)
-// (R3 upper trapezoidal, stored in lastT with ld n3): the slice block of
-// the TSQR, written at row offset row0 of B.
-__device__ void times_r3t(double* out, int ldo, const double* X, int ldxp, int rows, int ncol,
-                          int R2, const double* lastT, int n3) {
-  for (int e = threadIdx.x; e < rows * ncol; e += NT) {
-    const int r = e % rows, c = e / rows;
-    double s0 = 0.0, s1 = 0.0;
-    int b = c;
-    for (; b + 1 < R2; b += 2) {
-      s0 += X[r + ldxp * b] * lastT[c + n3 * b];
-      s1 += X[r + ldxp * (b + 1)] * lastT[c + n3 * (b + 1)];
+// out(r, c) = sum_{b >= c} X(r, b) R3(c, b) for r < rows, c < ncol, with
+// R3 upper trapezoidal in lastT (ld n3); out index r + ldo*c, or c + ldo*r
+// when trans.  4-row strips per thread.
+__device__ void times_r3t(double* out, int ldo, bool trans, const double* X, int ldxp, int rows,
+                          int ncol, int R2, const double* lastT, int n3) {
+  const int ngr = (rows + 3) >> 2;
+  for2d(ngr, ncol, [&](int ig, int c) {
+    const int r0 = ig << 2;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const int nr = min(4, rows - r0);
+    if (nr == 4) {
+      for (int b = c; b < R2; ++b) {
+        const double l = lastT[c + n3 * b];
+        const double* xp = X + r0 + ldxp * b;
+        a0 += xp[0] * l;
+        a1 += xp[1] * l;
+        a2 += xp[2] * l;
+        a3 += xp[3] * l;
+      }
+    } else {
+      for (int b = c; b < R2; ++b) {
+        const double l = lastT[c + n3 * b];
+        const double* xp = X + r0 + ldxp * b;
+        a0 += xp[0] * l;
+        if (nr > 1) a1 += xp[1] * l;
+        if (nr > 2) a2 += xp[2] * l;
+      }
     }
-    if (b < R2) s0 += X[r + ldxp * b] * lastT[c + n3 * b];
-    out[r + ldo * c] = s0 + s1;
-  }
+    const double acc[4] = {a0, a1, a2, a3};
+    for (int u = 0; u < nr; ++u) {
+      const int r = r0 + u;
+      out[trans ? (c + ldo * r) : (r + ldo * c)] = acc[u];
+    }
+  });
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
+template <bool SMALL>
+__global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs p) {
   extern __shared__ double sm[];
   const int n1 = p.n1, n2 = p.n2, n3 = p.n3;
   const int mx = max(n1, n3);
@@ -523,7 +657,8 @@ __global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
   double* U1 = XP + n1 * RMX;              // n1 x n1
   double* Xs = U1 + n1 * n1;               // mx x mx
   double* Ms = Xs + mx * mx;               // p.MSMAX
-  double* sig = Ms + p.MSMAX;              // mx
+  double* vbuf = Ms + p.MSMAX;             // 2 x HMAX
+  double* sig = vbuf + 2 * HMAX;           // mx
   double* sraw = sig + mx;                 // mx
   double* vn = sraw + mx;                  // mx
   double* sh = vn + mx;                    // 32 scalars
@@ -585,21 +720,19 @@ __global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
   // ---- materialise F (n1 x R1) and last^T (n3 x R2) ----
   for (int k = 0; k < K; ++k) {
     const TermInfo& t = terms[k];
-    for (int e = threadIdx.x; e < n1 * t.r1; e += NT) {
-      const int i = e % n1, a = e / n1;
+    for2d(n1, t.r1, [&](int i, int a) {
       const int ii = t.refl == 1 ? n1 - 1 - i : i;
       double v = t.scale * t.base[ii + n1 * a];
       if (t.u[0]) v *= t.u[0][i];
       F[i + n1 * (t.off1 + a)] = v;
-    }
+    });
     const double* L = t.base + (long long)n1 * t.r1 + (long long)n2 * t.r1 * t.r2;
-    for (int e = threadIdx.x; e < n3 * t.r2; e += NT) {
-      const int b = e % t.r2, kk = e / t.r2;  // coalesced read of last (b fastest)
+    for2d(t.r2, n3, [&](int b, int kk) {  // coalesced read of last (b fastest)
       const int kr = t.refl == 3 ? n3 - 1 - kk : kk;
       double v = L[b + t.r2 * kr];
       if (t.u[2]) v *= t.u[2][kk];
       lastT[kk + n3 * (t.off2 + b)] = v;
-    }
+    });
   }
   __syncthreads();
   PROF(0);
@@ -624,33 +757,22 @@ __global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
         // T_j^T block: B(row0 + c, i) = sum_b X(i, b) R3(c, b), X = F M_j
         left_times_blockdiag(XP, n1, F, n1, n1, R2, Ms, terms, colterm);
         __syncthreads();
-        for (int e = threadIdx.x; e < q3 * n1; e += NT) {
-          const int c = e % q3, i = e / q3;
-          double s0 = 0.0, s1 = 0.0;
-          int b = c;
-          for (; b + 1 < R2; b += 2) {
-            s0 += XP[i + n1 * b] * lastT[c + n3 * b];
-            s1 += XP[i + n1 * (b + 1)] * lastT[c + n3 * (b + 1)];
-          }
-          if (b < R2) s0 += XP[i + n1 * b] * lastT[c + n3 * b];
-          B[row0 + c + HMAX * i] = s0 + s1;
-        }
+        times_r3t(B + row0, HMAX, true, XP, n1, n1, q3, R2, lastT, n3);
       } else {
         // (M_j R3^T)^T block: B(row0 + c, off1 + a) = sum_b R3(c, off2 + b) M_t(a, b)
-        for (int e = threadIdx.x; e < q3 * R1; e += NT) {
-          const int c = e % q3, col = e / q3;
+        for2d(q3, R1, [&](int c, int col) {
           const TermInfo& t = terms[rowterm[col]];
           const int a = col - t.off1;
           double s = 0.0;
           for (int b = max(0, c - t.off2); b < t.r2; ++b)
             s += lastT[c + n3 * (t.off2 + b)] * Ms[t.ms + a + t.r1 * b];
           B[row0 + c + HMAX * col] = s;
-        }
+        });
       }
     }
     __syncthreads();
     PROF(2);
-    qr_update(Rr, mx, B, HMAX, (jn - j0) * q3, c1, sh);
+    qr_update<SMALL>(Rr, mx, B, HMAX, (jn - j0) * q3, c1, vbuf, HMAX, sh);
     PROF(3);
   }
   __syncthreads();
@@ -662,21 +784,20 @@ __global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
     Mc = Rr;  // C^T = R_T
     ldmc = mx;
   } else {
-    for (int e = threadIdx.x; e < c1 * n1; e += NT) {  // C^T = R2 F^T
-      const int pp = e % c1, i = e / c1;
+    for2d(c1, n1, [&](int pp, int i) {  // C^T = R2 F^T
       double v = 0.0;
       for (int a = pp; a < R1; ++a) v += Rr[pp + mx * a] * F[i + n1 * a];
       B[pp + HMAX * i] = v;
-    }
+    });
     Mc = B;
     ldmc = HMAX;
   }
   __syncthreads();
   double loc = 0.0;
-  for (int e = threadIdx.x; e < c1 * n1; e += NT) {
-    const double v = Mc[(e % c1) + ldmc * (e / c1)];
+  for2d(c1, n1, [&](int pp, int i) {
+    const double v = Mc[pp + ldmc * i];
     loc += v * v;
-  }
+  });
   const double norm2 = block_sum(loc, sh + 8);
   if (norm2 == 0.0 || !isfinite(norm2)) {
     // canonical zero, TtTensor::constant(n1, n2, n3, 0) (reference :168)
@@ -706,19 +827,18 @@ __global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
     return;
   }
   const double budget2 = p.eps * p.eps * norm2 / 2.0;
-  const SvdWork sw{Xs, vn, sig, sraw, piv, perm, sh, mx};
+  const SvdWork sw{p.prof, Xs, vn, sig, sraw, piv, perm, sh, mx};
   PROF(4);
   double mg1 = 0.0;
   const int t1 = svd_left(Mc, ldmc, c1, n1, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
   if (p.margins && threadIdx.x == 0) p.margins[2 * o] = mg1;
   PROF(5);
   // P = U1^T F (t1 x R1) into XP (ld n1)
-  for (int e = threadIdx.x; e < t1 * R1; e += NT) {
-    const int r = e % t1, col = e / t1;
+  for2d(t1, R1, [&](int r, int col) {
     double s = 0.0;
     for (int i = 0; i < n1; ++i) s += U1[i + n1 * r] * F[i + n1 * col];
     XP[r + n1 * col] = s;
-  }
+  });
 
   // ---- 4. cut 2 TSQR over S_j = P blockdiag(M_j) R3^T (t1 x q3) ----
   for (int e = threadIdx.x; e < mx * mx; e += NT) Rr[e] = 0.0;
@@ -733,11 +853,11 @@ __global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
       __syncthreads();
       left_times_blockdiag(X2, n1, XP, n1, t1, R2, Ms, terms, colterm);
       __syncthreads();
-      times_r3t(B + row0, HMAX, X2, n1, t1, q3, R2, lastT, n3);
+      times_r3t(B + row0, HMAX, false, X2, n1, t1, q3, R2, lastT, n3);
     }
     __syncthreads();
     PROF(6);
-    qr_update(Rr, mx, B, HMAX, (jn - j0) * t1, q3, sh);
+    qr_update<SMALL>(Rr, mx, B, HMAX, (jn - j0) * t1, q3, vbuf, HMAX, sh);
     PROF(7);
   }
   __syncthreads();
@@ -776,43 +896,37 @@ __global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
   // ---- 5. outputs ----
   for (int e = threadIdx.x; e < n1 * t1; e += NT) dst[e] = U1[e];
   // W2 = V2 (q3 x t2) from B into Rr (ld mx); G = [W2; 0] into Xs (ld mx)
-  for (int e = threadIdx.x; e < n3 * t2; e += NT) {
-    const int c = e % n3, s = e / n3;
+  for2d(n3, t2, [&](int c, int s) {
     const double v = c < q3 ? B[c + HMAX * s] : 0.0;
     Xs[c + mx * s] = v;
     if (c < q3) Rr[c + mx * s] = v;
-  }
+  });
   __syncthreads();
   // Z = R3^T W2 (R2 x t2, ld BROWS) into B
   double* Z = B;
-  for (int e = threadIdx.x; e < R2 * t2; e += NT) {
-    const int b = e % R2, s = e / R2;
+  for2d(R2, t2, [&](int b, int s) {
     double acc = 0.0;
     const int cm = min(b, q3 - 1);
     for (int c = 0; c <= cm; ++c) acc += lastT[c + n3 * b] * Rr[c + mx * s];
     Z[b + BROWS * s] = acc;
-  }
-  // last = (Q3 G)^T, Q3 = H_0 ... H_{q3-1}
+  });
+  // last = (Q3 G)^T, Q3 = H_0 ... H_{q3-1}: columns of G are independent,
+  // one thread applies every reflector to its column
   const int kmax = min(n3, R2);
-  for (int k = kmax - 1; k >= 0; --k) {
-    const double t = tau[k];
-    __syncthreads();
-    if (t != 0.0) {
-      for (int s = threadIdx.x; s < t2; s += NT) {
-        double* g = Xs + mx * s;
-        double w = g[k];
-        for (int i = k + 1; i < n3; ++i) w += lastT[i + n3 * k] * g[i];
-        w *= t;
-        g[k] -= w;
-        for (int i = k + 1; i < n3; ++i) g[i] -= w * lastT[i + n3 * k];
-      }
+  for (int s = threadIdx.x; s < t2; s += NT) {
+    double* g = Xs + mx * s;
+    for (int k = kmax - 1; k >= 0; --k) {
+      const double t = tau[k];
+      if (t == 0.0) continue;
+      double w = g[k];
+      for (int i = k + 1; i < n3; ++i) w += lastT[i + n3 * k] * g[i];
+      w *= t;
+      g[k] -= w;
+      for (int i = k + 1; i < n3; ++i) g[i] -= w * lastT[i + n3 * k];
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < t2 * n3; e += NT) {
-    const int s = e % t2, kk = e / t2;
-    dlast[s + t2 * kk] = Xs[kk + mx * s];
-  }
+  for2d(t2, n3, [&](int s, int kk) { dlast[s + t2 * kk] = Xs[kk + mx * s]; });
   // middle_j = (P blockdiag(M_j)) Z
   for (int j = 0; j < n2; ++j) {
     __syncthreads();
@@ -820,8 +934,7 @@ __global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
     __syncthreads();
     left_times_blockdiag(X2, n1, XP, n1, t1, R2, Ms, terms, colterm);
     __syncthreads();
-    for (int e = threadIdx.x; e < t1 * t2; e += NT) {
-      const int r = e % t1, s = e / t1;
+    for2d(t1, t2, [&](int r, int s) {
       double a0 = 0.0, a1 = 0.0;
       int b = 0;
       for (; b + 1 < R2; b += 2) {
@@ -830,7 +943,7 @@ __global__ void __launch_bounds__(NT, 4) round_sums_kernel(RoundArgs p) {
       }
       if (b < R2) a0 += X2[r + n1 * b] * Z[b + BROWS * s];
       dmid[(long long)j * t1 * t2 + r + t1 * s] = a0 + a1;
-    }
+    });
   }
   __syncthreads();
   PROF(10);
@@ -844,7 +957,8 @@ size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int 
   const size_t RMX = RM1 > RM2 ? RM1 : RM2;
   const size_t BROWS = HMAX > RM2 ? HMAX : RM2;
   size_t d = (size_t)n1 * RMX + (size_t)n3 * RM2 + mx + mx * mx + BROWS * mx +
-             (size_t)n1 * RMX + (size_t)n1 * n1 + mx * mx + (size_t)MSMAX + 3 * mx + 32;
+             (size_t)n1 * RMX + (size_t)n1 * n1 + mx * mx + (size_t)MSMAX + 2 * (size_t)HMAX +
+             3 * mx + 32;
   size_t ints = 2 * mx + RM2 + RM1 + 1;
   size_t bytes = d * 8 + ((ints * 4 + 7) / 8) * 8 + sizeof(TermInfo) * kMaxTerms + 64;
   return bytes;
@@ -881,10 +995,16 @@ cudaError_t launch_round_bounds(const RoundArgs& a, int* bounds, cudaStream_t st
 cudaError_t launch_round(const RoundArgs& a, cudaStream_t st) {
   if (a.nout == 0) return cudaSuccess;
   const size_t smem = round_smem_bytes(a.n1, a.n2, a.n3, a.RM1, a.RM2, a.HMAX, a.MSMAX);
-  cudaError_t e = cudaFuncSetAttribute(round_sums_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const bool small = a.n1 <= 32 && a.n3 <= 32 && a.HMAX <= 32;
+  cudaError_t e = small ? cudaFuncSetAttribute(round_sums_kernel<true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                        : cudaFuncSetAttribute(round_sums_kernel<false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  round_sums_kernel<<<a.nout, NT, smem, st>>>(a);
+  if (small)
+    round_sums_kernel<true><<<a.nout, NT, smem, st>>>(a);
+  else
+    round_sums_kernel<false><<<a.nout, NT, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -25,8 +25,13 @@ if os.environ.get("ROUND_PROF"):
     names = ["load", "qr_last", "cut1_blocks", "cut1_qrupd", "C+norm", "jacobi1", "cut2_blocks",
              "cut2_qrupd", "P..", "jacobi2", "output"]
     tot = cyc.sum()
+    tot = cyc[:11].sum()
     print("round phases (% of thread-0 cycles):",
           {names[i]: round(100 * cyc[i] / tot, 1) for i in range(11)})
+    nr = max(1, cyc[13] / 2)
+    print("mean kcycles per rounding:", {names[i]: round(cyc[i] / nr / 1e3, 1) for i in range(11)},
+          "total", round(tot / nr / 1e3, 1))
+    print("jacobi: %d svds, mean sweeps %.2f, hit cap %d" % (cyc[13], cyc[12] / max(1, cyc[13]), cyc[14]))
 print(f"{p.name} scale {a.scale}: {p.mesh.ncell} cells, {a.steps} steps, {ms:.2f} ms, "
       f"launches {ctx.launch_count()}")
 ctx.close()
