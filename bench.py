@@ -219,16 +219,56 @@ def main():
     from paper_1912_04582_b200.problems import config
     p = config(args.config, args.scale)
     ctx = Context(local)
-    ctx.setup(p)
+    part = None
+    if world > 1:
+        # weak scaling: the global periodic box is `world` x-slabs of the
+        # single-GPU workload; each rank owns one slab plus its halo ghosts
+        from paper_1912_04582_b200 import halo
+        from paper_1912_04582_b200.partition import build_part, local_state
+        from paper_1912_04582_b200.problems import periodic_box
+        nx, ny, nz = p.mesh.shape
+        pg = periodic_box((nx * world, ny, nz), nv=p.nv, bound=p.bound, eps=p.eps, cap=p.cap,
+                          name=p.name + f"-x{world}")
+        from paper_1912_04582_b200.mesh import slab_partition
+        part = build_part(pg.mesh, slab_partition(pg.mesh, world), rank)
+        ctx.set_grid(pg.nv, pg.bound)
+        ctx.set_gas(pg.gas)
+        ctx.set_mesh(part.mesh)
+        ctx.set_bcs(pg.bcs)
+        ctx.set_owned(part.n_owned)
+        f_local = local_state(part, pg.f0)
+        ctx.upload_state(f_local)
+        pack, unpack = halo.gpu_pack_unpack(ctx, torch.device("cuda", local))
+        p = pg
+        cells_per_rank = part.n_owned
+    else:
+        ctx.setup(p)
+        f_local = p.f0
+        cells_per_rank = p.mesh.ncell
     fp64_peak = ctx.fp64_peak()
-    ctx.step(p.dt, p.eps, p.cap, args.warmup)
-    ctx.upload_state(p.f0)  # time steps 1..K from the initial state
+
+    def run_steps(k):
+        if part is None:
+            return ctx.timed_step(p.dt, p.eps, p.cap, k)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(k):
+            ctx.step(p.dt, p.eps, p.cap, 1)
+            halo.exchange(part, pack, unpack, p.nv, device=torch.device("cuda", local))
+        ev1.record()
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1)
+
+    run_steps(args.warmup)
+    ctx.upload_state(f_local)  # time steps 1..K from the initial state
     ctx.set_profiling(True)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        ms = ctx.timed_step(p.dt, p.eps, p.cap, args.steps)
+        ms = run_steps(args.steps)
     torch.cuda.synchronize()
     phase_ms = ctx.phase_times()
     flops, bytes_, launches = ctx.phase_work()
@@ -239,14 +279,14 @@ def main():
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    cells = p.mesh.ncell
+    cells = cells_per_rank
     value = world * cells * args.steps / (ms / 1e3)
 
     # e2e through the public API with host buffers: upload state, one step,
     # download state -- every step
     ctx.set_profiling(False)
     # (the host state advances: steps 1..E from the initial state, as timed)
-    host = p.f0
+    host = f_local
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
@@ -255,6 +295,8 @@ def main():
         h2d += int(host.cores.nbytes + host.ranks.nbytes + host.offsets.nbytes)
         ctx.upload_state(host)
         ctx.step(p.dt, p.eps, p.cap, 1)
+        if part is not None:
+            halo.exchange(part, pack, unpack, p.nv, device=torch.device("cuda", local))
         host = ctx.download_state()
         d2h += int(host.cores.nbytes + host.ranks.nbytes + host.offsets.nbytes)
     h2d //= args.e2e_steps
@@ -299,7 +341,10 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": dict(workload_config(p, args),
-                                                    parallelism=f"replicas x{world}",
+                                                    parallelism=(f"x-slab partition x{world}, "
+                                                                 "halo TT cores over NCCL"
+                                                                 if world > 1 else "single GPU"),
+                                                    cells_per_gpu=cells_per_rank,
                                                     max_rank_after=max_rank),
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "cell-steps/s", "h2d_bytes_per_step": h2d,

@@ -95,8 +95,23 @@ int ttdvm_cuda_download_state(ttdvm_ctx* ctx, double* cores, int64_t capacity);
  * the reference). */
 int ttdvm_cuda_step(ttdvm_ctx* ctx, double dt, double eps, int32_t cap, int32_t nsteps);
 
+/* Multi-GPU slab partition: cells [0, nowned) of the
+ * mesh are stepped, the rest are halo ghosts whose states the caller
+ * refreshes after every step with the two calls below (packed in the
+ * ttdvm_tt_batch layout into / out of caller-provided DEVICE buffers that
+ * the caller exchanges with NCCL).  Ghosts carry over unchanged otherwise. */
+int ttdvm_cuda_set_owned(ttdvm_ctx* ctx, int32_t nowned);
+/* Pack the current states of cells ids[0..count) into dev_dst; fills
+ * ranks_out[2*count] and offsets_out[count+1] (doubles).  ENOMEM with
+ * offsets_out[count] = required size if capacity is too small. */
+int ttdvm_cuda_halo_pack(ttdvm_ctx* ctx, int32_t count, const int32_t* ids, int32_t* ranks_out,
+                         int64_t* offsets_out, double* dev_dst, int64_t capacity);
+/* Install received ghost states (ranks / offsets as produced by pack). */
+int ttdvm_cuda_halo_unpack(ttdvm_ctx* ctx, int32_t count, const int32_t* ids,
+                           const int32_t* ranks, const int64_t* offsets, const double* dev_src);
+
 /* Macroparameters of the state the last step started from
- * (compute_macro, proj/src/physics.cpp:17-67), 11 doubles per cell:
+ * (compute_macro, proj/src/physics.cpp:17-67), 11 doubles per owned cell:
  * n, u0, u1, u2, T, rho, p, S0, S1, S2, nu (= p / mu(T)). */
 int ttdvm_cuda_macros(ttdvm_ctx* ctx, double* out);
 

@@ -41,6 +41,12 @@ cudaError_t launch_shakhov_raw(const double* macro, int count, int n, const doub
 cudaError_t launch_gather(const TSet& s, int count, const long long* dst_off, int n1, int n2,
                           int n3, double* dst, cudaStream_t st);
 cudaError_t launch_dfma_probe(double* out, int blocks, int threads, int iters, cudaStream_t st);
+cudaError_t launch_place(const TSet& s, const int* src_ids, int count, int n1, int n2, int n3,
+                         int* dst_ranks, long long* dst_off, const int* dst_ids,
+                         const long long* new_off, double* dst_base, cudaStream_t st);
+cudaError_t launch_gather_ids(const TSet& s, const int* src_ids, int count,
+                              const long long* dst_off, int n1, int n2, int n3, double* dst,
+                              cudaStream_t st);
 }  // namespace ttdvm
 
 using namespace ttdvm;
@@ -156,6 +162,7 @@ struct ttdvm_ctx {
   double gas[6] = {1.0, 0.5, 2.0 / 3.0, 1.0, 1.0, 0.5};
   // mesh
   int ncell = 0, nface = 0;
+  int nowned = -1;  // cells [0, nowned) are stepped; the rest are halo ghosts
   std::vector<int> left, right, group;
   std::vector<double> area, normal, volume;
   std::vector<long long> cfo;
@@ -375,11 +382,11 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   throw Fail{TTDVM_ENOMEM, "rounding arena could not be grown"};
 }
 
-void run_macro(ttdvm_ctx* c, TensorSet& s, double* macro, double* nu) {
+void run_macro(ttdvm_ctx* c, TensorSet& s, double* macro, double* nu, int count = -1) {
   ensure_static(c);
   MacroArgs a;
   a.set = s.view();
-  a.count = s.count;
+  a.count = count < 0 ? s.count : count;
   a.n = c->n;
   a.nodes = c->d_nodes.p;
   a.weights = c->d_weights.p;
@@ -402,14 +409,14 @@ void run_macro(ttdvm_ctx* c, TensorSet& s, double* macro, double* nu) {
 }
 
 // collision of `s` (set 0): f_S raw -> round -> (f_S - f) round; J_r in c->jr
-void run_collision(ttdvm_ctx* c, TensorSet& s, double eps) {
-  const int count = s.count;
+void run_collision(ttdvm_ctx* c, TensorSet& s, double eps, int count_ = -1) {
+  const int count = count_ < 0 ? s.count : count_;
   const int n = c->n;
   c->d_macro.alloc(std::max(1, 11 * count));
   c->d_nu.alloc(std::max(1, count));
   {
     Timer t(c, 0);
-    run_macro(c, s, c->d_macro.p, c->d_nu.p);
+    run_macro(c, s, c->d_macro.p, c->d_nu.p, count);
   }
   {
     Timer t(c, 1);
@@ -562,10 +569,11 @@ void build_step_terms(ttdvm_ctx* c) {
   }
   fl.upload();
   // residual: R_i = round(J_i + sum_j Phi_j * (-s A_j / V_i))
+  const int nown = c->nowned < 0 ? c->ncell : c->nowned;
   TermList& rl = c->t_res;
   rl.off.assign(1, 0);
   rl.terms.clear();
-  for (int i = 0; i < c->ncell; ++i) {
+  for (int i = 0; i < nown; ++i) {
     rl.terms.push_back(Term{S_JR, i, 1.0, -1, 0});
     for (long long e = c->cfo[i]; e < c->cfo[i + 1]; ++e) {
       const int fid = c->cfid[e];
@@ -578,10 +586,10 @@ void build_step_terms(ttdvm_ctx* c) {
   rl.upload();
   // update: f_i' = round(f_i + R_i * dt)   (dt is the uniform scale of R)
   TermList& ul = c->t_upd;
-  ul.off.resize(c->ncell + 1);
-  ul.terms.resize(2 * (size_t)c->ncell);
-  for (int i = 0; i <= c->ncell; ++i) ul.off[i] = 2LL * i;
-  for (int i = 0; i < c->ncell; ++i) {
+  ul.off.resize(nown + 1);
+  ul.terms.resize(2 * (size_t)nown);
+  for (int i = 0; i <= nown; ++i) ul.off[i] = 2LL * i;
+  for (int i = 0; i < nown; ++i) {
     ul.terms[2 * i] = Term{S_STATE, i, 1.0, -1, 0};
     ul.terms[2 * i + 1] = Term{S_RES, i, 1.0, -1, 0};
   }
@@ -589,12 +597,57 @@ void build_step_terms(ttdvm_ctx* c) {
   c->terms_dirty = false;
 }
 
+// Grow an arena to hold `need` doubles, preserving its first `keep` doubles.
+void grow_preserve(ttdvm_ctx* c, TensorSet& s, long long keep, long long need) {
+  if ((long long)s.arena.n >= need) return;
+  DevBuf<double> nb;
+  nb.alloc((size_t)std::max<long long>(need, (long long)(s.arena.n * 3 / 2)));
+  if (keep > 0) CK(cudaMemcpyAsync(nb.p, s.arena.p, 8LL * keep, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  s.arena.free();
+  s.arena = nb;
+  nb.p = nullptr;
+  nb.n = 0;
+}
+
+// Append tensors (src set, src_ids on device or null = 0..count-1) to the
+// arena of dst as entries dst_ids (host); ranks_host gives their ranks.
+void append_tensors(ttdvm_ctx* c, const TSet& src, const int* src_ids_dev, int count,
+                    const int* ranks_host, const int* dst_ids_host, TensorSet& dst) {
+  if (count == 0) return;
+  std::vector<long long> off(count);
+  long long at = dst.used;
+  int m1 = dst.maxr1, m2 = dst.maxr2;
+  for (int i = 0; i < count; ++i) {
+    off[i] = at;
+    at += tt_size(c->n, c->n, c->n, ranks_host[2 * i], ranks_host[2 * i + 1]);
+    m1 = std::max(m1, ranks_host[2 * i]);
+    m2 = std::max(m2, ranks_host[2 * i + 1]);
+  }
+  grow_preserve(c, dst, dst.used, at);
+  c->d_tmp_off.alloc(count);
+  CK(cudaMemcpy(c->d_tmp_off.p, off.data(), 8LL * count, cudaMemcpyHostToDevice));
+  DevBuf<int> ids;
+  ids.alloc(count);
+  CK(cudaMemcpy(ids.p, dst_ids_host, 4LL * count, cudaMemcpyHostToDevice));
+  CK(launch_place(src, src_ids_dev, count, c->n, c->n, c->n, dst.ranks.p, dst.off.p, ids.p,
+                  c->d_tmp_off.p, dst.arena.p, c->st));
+  c->launches += 1;
+  CK(cudaStreamSynchronize(c->st));
+  ids.free();
+  dst.used = at;
+  dst.maxr1 = m1;
+  dst.maxr2 = m2;
+}
+
 void step_once(ttdvm_ctx* c, double dt, double eps, int cap) {
   TensorSet& s = c->state[c->cur];
   TensorSet& nxt = c->state[1 - c->cur];
-  // pieces (3) + (4): moments, f_S, J_r = round(f_S - f); nu applied as
-  // J's per-tensor scale (TtTensor::scaled after rounding, physics.cpp:118)
-  run_collision(c, s, eps);
+  const int nown = c->nowned < 0 ? c->ncell : c->nowned;
+  // pieces (3) + (4): moments, f_S, J_r = round(f_S - f) over the owned
+  // cells; nu applied as J's per-tensor scale (TtTensor::scaled after
+  // rounding, physics.cpp:118)
+  run_collision(c, s, eps, nown);
   c->jr.tscale = c->d_nu.p;
   TensorSet* sets[kMaxSets] = {&s, &c->fsraw, &c->fs, &c->jr, &c->phi, &c->res, &c->freestream, &c->in};
   {
@@ -607,11 +660,25 @@ void step_once(ttdvm_ctx* c, double dt, double eps, int cap) {
     run_round(c, c->t_res, sets, c->res, eps, cap, nullptr);
   }
   c->res.uscale = dt;
+  nxt.resize(c->ncell);
   {
     Timer t(c, 6);
     run_round(c, c->t_upd, sets, nxt, eps, cap, nullptr);
   }
   c->res.uscale = 1.0;
+  nxt.count = c->ncell;
+  if (nown < c->ncell) {
+    // ghosts carry over unchanged until a halo exchange replaces them
+    const int ng = c->ncell - nown;
+    std::vector<int> rk(2 * (size_t)ng), ids(ng);
+    CK(cudaMemcpy(rk.data(), s.ranks.p + 2LL * nown, 8LL * ng, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < ng; ++i) ids[i] = nown + i;
+    DevBuf<int> sid;
+    sid.alloc(ng);
+    CK(cudaMemcpy(sid.p, ids.data(), 4LL * ng, cudaMemcpyHostToDevice));
+    append_tensors(c, s.view(), sid.p, ng, rk.data(), ids.data(), nxt);
+    sid.free();
+  }
   c->cur = 1 - c->cur;
 }
 
@@ -801,7 +868,8 @@ int ttdvm_cuda_step(ttdvm_ctx* c, double dt, double eps, int32_t cap, int32_t ns
 int ttdvm_cuda_macros(ttdvm_ctx* c, double* out) {
   return guard(c, [&] {
     require(c->d_macro.p != nullptr, "no step has run");
-    CK(cudaMemcpy(out, c->d_macro.p, 8LL * 11 * c->ncell, cudaMemcpyDeviceToHost));
+    const int nown = c->nowned < 0 ? c->ncell : c->nowned;
+    CK(cudaMemcpy(out, c->d_macro.p, 8LL * 11 * nown, cudaMemcpyDeviceToHost));
   });
 }
 
@@ -913,6 +981,71 @@ int ttdvm_cuda_collision_batch(ttdvm_ctx* c, const ttdvm_tt_batch* in, double ep
 int ttdvm_cuda_phase_times(ttdvm_ctx* c, double* ms8) {
   return guard(c, [&] {
     for (int i = 0; i < 8; ++i) ms8[i] = c->phase_ms[i];
+  });
+}
+
+int ttdvm_cuda_set_owned(ttdvm_ctx* c, int32_t nowned) {
+  return guard(c, [&] {
+    require(nowned >= 1 && nowned <= c->ncell, "owned cell count out of range");
+    c->nowned = nowned;
+    c->terms_dirty = true;
+  });
+}
+
+int ttdvm_cuda_halo_pack(ttdvm_ctx* c, int32_t count, const int32_t* ids, int32_t* ranks_out,
+                         int64_t* offsets_out, double* dev_dst, int64_t capacity) {
+  return guard(c, [&] {
+    TensorSet& s = c->state[c->cur];
+    std::vector<int> all(2 * (size_t)s.count);
+    if (s.count) CK(cudaMemcpy(all.data(), s.ranks.p, all.size() * 4, cudaMemcpyDeviceToHost));
+    long long o = 0;
+    std::vector<long long> off(std::max(1, count));
+    for (int i = 0; i < count; ++i) {
+      require(ids[i] >= 0 && ids[i] < s.count, "halo id out of range");
+      ranks_out[2 * i] = all[2 * ids[i]];
+      ranks_out[2 * i + 1] = all[2 * ids[i] + 1];
+      off[i] = o;
+      offsets_out[i] = o;
+      o += tt_size(c->n, c->n, c->n, ranks_out[2 * i], ranks_out[2 * i + 1]);
+    }
+    offsets_out[count] = o;
+    if (o > capacity)
+      throw Fail{TTDVM_ENOMEM, "halo buffer too small: need " + std::to_string(o) + " doubles"};
+    if (count == 0) return;
+    DevBuf<int> did;
+    did.alloc(count);
+    CK(cudaMemcpy(did.p, ids, 4LL * count, cudaMemcpyHostToDevice));
+    c->d_tmp_off.alloc(count);
+    CK(cudaMemcpy(c->d_tmp_off.p, off.data(), 8LL * count, cudaMemcpyHostToDevice));
+    CK(launch_gather_ids(s.view(), did.p, count, c->d_tmp_off.p, c->n, c->n, c->n, dev_dst, c->st));
+    c->launches += 1;
+    CK(cudaStreamSynchronize(c->st));
+    did.free();
+  });
+}
+
+int ttdvm_cuda_halo_unpack(ttdvm_ctx* c, int32_t count, const int32_t* ids, const int32_t* ranks,
+                           const int64_t* offsets, const double* dev_src) {
+  return guard(c, [&] {
+    TensorSet& s = c->state[c->cur];
+    if (count == 0) return;
+    for (int i = 0; i < count; ++i)
+      require(ids[i] >= 0 && ids[i] < s.count, "halo id out of range");
+    DevBuf<int> rk;
+    DevBuf<long long> of;
+    rk.alloc(2 * (size_t)count);
+    of.alloc(count);
+    CK(cudaMemcpy(rk.p, ranks, 8LL * count, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(of.p, offsets, 8LL * count, cudaMemcpyHostToDevice));
+    TSet src;
+    src.ranks = rk.p;
+    src.off = of.p;
+    src.base = dev_src;
+    src.tscale = nullptr;
+    src.uscale = 1.0;
+    append_tensors(c, src, nullptr, count, ranks, ids, s);
+    rk.free();
+    of.free();
   });
 }
 

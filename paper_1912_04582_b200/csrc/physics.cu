@@ -274,6 +274,58 @@ __global__ void gather_kernel(TSet s, int count, const long long* dst_off, int n
   for (long long e = threadIdx.x; e < sz; e += blockDim.x) d[e] = src[e];
 }
 
+// Copy tensors src_ids[i] of a set to dst_base + new_off[i] and register
+// them as entries dst_ids[i] of the destination set (halo unpack / ghost
+// carry-over).
+__global__ void place_kernel(TSet s, const int* src_ids, int count, int n1, int n2, int n3,
+                             int* dst_ranks, long long* dst_off, const int* dst_ids,
+                             const long long* new_off, double* dst_base) {
+  const int i = blockIdx.x;
+  if (i >= count) return;
+  const int t = src_ids ? src_ids[i] : i;
+  const int r1 = s.ranks[2 * t], r2 = s.ranks[2 * t + 1];
+  const long long sz = (long long)n1 * r1 + (long long)n2 * r1 * r2 + (long long)r2 * n3;
+  const double* src = s.base + s.off[t];
+  double* d = dst_base + new_off[i];
+  for (long long e = threadIdx.x; e < sz; e += blockDim.x) d[e] = src[e];
+  if (threadIdx.x == 0) {
+    const int di = dst_ids[i];
+    dst_ranks[2 * di] = r1;
+    dst_ranks[2 * di + 1] = r2;
+    dst_off[di] = new_off[i];
+  }
+}
+
+cudaError_t launch_place(const TSet& s, const int* src_ids, int count, int n1, int n2, int n3,
+                         int* dst_ranks, long long* dst_off, const int* dst_ids,
+                         const long long* new_off, double* dst_base, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  place_kernel<<<count, 128, 0, st>>>(s, src_ids, count, n1, n2, n3, dst_ranks, dst_off, dst_ids,
+                                      new_off, dst_base);
+  return cudaGetLastError();
+}
+
+// Gather tensors src_ids[i] (or i) of a set into dst + dst_off[i].
+__global__ void gather_ids_kernel(TSet s, const int* src_ids, int count, const long long* dst_off,
+                                  int n1, int n2, int n3, double* dst) {
+  const int i = blockIdx.x;
+  if (i >= count) return;
+  const int t = src_ids[i];
+  const int r1 = s.ranks[2 * t], r2 = s.ranks[2 * t + 1];
+  const long long sz = (long long)n1 * r1 + (long long)n2 * r1 * r2 + (long long)r2 * n3;
+  const double* src = s.base + s.off[t];
+  double* d = dst + dst_off[i];
+  for (long long e = threadIdx.x; e < sz; e += blockDim.x) d[e] = src[e];
+}
+
+cudaError_t launch_gather_ids(const TSet& s, const int* src_ids, int count,
+                              const long long* dst_off, int n1, int n2, int n3, double* dst,
+                              cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  gather_ids_kernel<<<count, 128, 0, st>>>(s, src_ids, count, dst_off, n1, n2, n3, dst);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gather(const TSet& s, int count, const long long* dst_off, int n1, int n2,
                           int n3, double* dst, cudaStream_t st) {
   if (count == 0) return cudaSuccess;

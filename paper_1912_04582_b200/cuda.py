@@ -32,6 +32,7 @@ EXPORTS = (
     "ttdvm_cuda_macro_batch", "ttdvm_cuda_collision_batch", "ttdvm_cuda_phase_times",
     "ttdvm_cuda_launch_count", "ttdvm_cuda_set_profiling", "ttdvm_cuda_phase_work",
     "ttdvm_cuda_timed_step", "ttdvm_cuda_fp64_peak", "ttdvm_cuda_round_profile",
+    "ttdvm_cuda_set_owned", "ttdvm_cuda_halo_pack", "ttdvm_cuda_halo_unpack",
 )
 
 OK, EINVAL, EDOMAIN, ENOMEM, ECUDA, ENCCL = range(6)
@@ -89,6 +90,9 @@ def load_library(path: str = LIB_PATH):
         "ttdvm_cuda_timed_step": (C.c_int, [vp, dbl, dbl, i32, i32, vp]),
         "ttdvm_cuda_fp64_peak": (C.c_int, [vp, vp]),
         "ttdvm_cuda_round_profile": (C.c_int, [vp, C.c_int, vp]),
+        "ttdvm_cuda_set_owned": (C.c_int, [vp, i32]),
+        "ttdvm_cuda_halo_pack": (C.c_int, [vp, i32, vp, vp, vp, vp, i64]),
+        "ttdvm_cuda_halo_unpack": (C.c_int, [vp, i32, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -212,8 +216,42 @@ class Context:
         """explicit_step, nsteps times, state resident."""
         self._check(self.lib.ttdvm_cuda_step(self.h, float(dt), float(eps), int(cap), int(nsteps)))
 
+    def set_owned(self, nowned: int):
+        """Cells [0, nowned) are stepped; the rest are halo ghosts."""
+        self._check(self.lib.ttdvm_cuda_set_owned(self.h, int(nowned)))
+        self.nowned = int(nowned)
+
+    def halo_pack(self, ids: np.ndarray, dev_ptr: int, capacity: int):
+        """Pack current states of local cells `ids` into the device buffer at
+        dev_ptr; returns (ranks [2k] int32, offsets [k+1] int64)."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        ranks = np.zeros(2 * max(len(ids), 1), dtype=np.int32)
+        offs = np.zeros(len(ids) + 1, dtype=np.int64)
+        self._check(self.lib.ttdvm_cuda_halo_pack(self.h, len(ids), _ptr(ids), _ptr(ranks),
+                                                  _ptr(offs), C.c_void_p(dev_ptr), int(capacity)))
+        return ranks[:2 * len(ids)], offs
+
+    def halo_size(self, ids: np.ndarray) -> int:
+        """Doubles needed to pack `ids` (pack with zero capacity)."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        ranks = np.zeros(2 * max(len(ids), 1), dtype=np.int32)
+        offs = np.zeros(len(ids) + 1, dtype=np.int64)
+        rc = self.lib.ttdvm_cuda_halo_pack(self.h, len(ids), _ptr(ids), _ptr(ranks), _ptr(offs),
+                                           None, 0)
+        if rc not in (OK, ENOMEM):
+            self._check(rc)
+        return int(offs[len(ids)])
+
+    def halo_unpack(self, ids: np.ndarray, ranks: np.ndarray, offs: np.ndarray, dev_ptr: int):
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        ranks = np.ascontiguousarray(ranks, dtype=np.int32)
+        offs = np.ascontiguousarray(offs, dtype=np.int64)
+        self._check(self.lib.ttdvm_cuda_halo_unpack(self.h, len(ids), _ptr(ids), _ptr(ranks),
+                                                    _ptr(offs), C.c_void_p(dev_ptr)))
+
     def macros(self) -> np.ndarray:
-        out = np.zeros((self.mesh.ncell, 11))
+        nown = getattr(self, "nowned", None) or self.mesh.ncell
+        out = np.zeros((nown, 11))
         self._check(self.lib.ttdvm_cuda_macros(self.h, _ptr(out)))
         return out
 
