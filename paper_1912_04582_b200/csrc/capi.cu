@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -24,6 +25,8 @@
 namespace ttdvm {
 cudaError_t launch_round(const RoundArgs& a, cudaStream_t st);
 cudaError_t launch_round_bounds(const RoundArgs& a, int* bounds, cudaStream_t st);
+cudaError_t launch_round_gram(const RoundArgs& a, cudaStream_t st);
+size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX);
 size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int MSMAX);
 struct MacroArgs {
   TSet set;
@@ -322,14 +325,24 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   const int mx = n;
   // TSQR block height: as tall as the shared-memory budget allows, aiming
   // at >= 3 resident CTAs per SM
-  // TSQR block height: n <= 32 runs the SMALL kernel (one slice per update,
-  // h <= 32, few registers, more resident CTAs); larger grids hold <= 48
-  // rows per update
-  if (mx > 48)
-    throw Fail{TTDVM_EINVAL, "velocity grids above 48 nodes per axis need the 256-thread "
-                             "rounding variant (not built yet)"};
-  const int HMAX = mx <= 32 ? mx : 48;
-  const size_t smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX, MSMAX);
+  // exact-Gram route by default; TTDVM_ROUND=tsqr selects the Householder
+  // TSQR route (kept for A/B comparison)
+  static const bool use_tsqr = [] {
+    const char* e = getenv("TTDVM_ROUND");
+    return e && std::string(e) == "tsqr";
+  }();
+  int HMAX = mx;
+  size_t smem;
+  if (use_tsqr) {
+    if (mx > 48)
+      throw Fail{TTDVM_EINVAL, "velocity grids above 48 nodes per axis are not supported"};
+    HMAX = mx <= 32 ? mx : 48;
+    smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX, MSMAX);
+  } else {
+    if (mx > 48)
+      throw Fail{TTDVM_EINVAL, "velocity grids above 48 nodes per axis are not supported"};
+    smem = round_gram_smem_bytes(n, n, RM1, RM2, MSMAX);
+  }
   if (smem > 227 * 1024)
     throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory (n=" + std::to_string(n) +
                                  ", summed ranks " + std::to_string(RM1) + "x" +
@@ -351,7 +364,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     a.out.capacity = (long long)out.arena.n;
     CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
     CK(cudaMemsetAsync(c->d_acc.p, 0, 2 * sizeof(double), c->st));
-    CK(launch_round(a, c->st));
+    CK(use_tsqr ? launch_round(a, c->st) : launch_round_gram(a, c->st));
     c->launches += 1;
     CK(cudaMemcpyAsync(c->h_status, c->d_status.p, (kStWords + 4) * sizeof(int),
                        cudaMemcpyDeviceToHost, c->st));

@@ -637,6 +637,214 @@ __device__ void times_r3t(double* out, int ldo, bool trans, const double* X, int
   });
 }
 
+// ---- double-double arithmetic for the exact Gram route -------------------
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+
+// (hi, lo) += a * b with the product and the sum error kept in lo
+__device__ __forceinline__ void dd_fma_acc(double& hi, double& lo, double a, double b) {
+  const double p = a * b;
+  const double pe = fma(a, b, -p);
+  double s, e;
+  two_sum(hi, p, s, e);
+  hi = s;
+  lo += e + pe;
+}
+
+__device__ __forceinline__ void dd_norm(double& hi, double& lo) {
+  double s, e;
+  two_sum(hi, lo, s, e);
+  hi = s;
+  lo = e;
+}
+
+// (a_hi, a_lo) * (b_hi, b_lo) -> (p, pe), unnormalised
+__device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl, double& p,
+                                       double& pe) {
+  p = ah * bh;
+  pe = fma(ah, bh, -p) + (ah * bl + al * bh);
+}
+
+// Visit the upper triangle (i <= j) of a d x d matrix: entry e -> (i, j).
+__device__ __forceinline__ void tri_index(int e, int d, int& i, int& j) {
+  int row = 0, len = d;
+  while (e >= len) {
+    e -= len;
+    ++row;
+    --len;
+  }
+  i = row;
+  j = row + e;
+}
+
+// Pivoted Cholesky of the symmetric PSD matrix G (d x d, hi/lo planes, ld
+// d) in double-double: Pi^T G Pi = R^T R, stopping when the largest
+// remaining pivot is <= thresh.  R (k x d, ld ldr, columns in pivoted
+// order) is rounded to double; piv[v] = original index of virtual column v.
+// Returns the rank k.
+__device__ int chol_piv_dd(double* Gh, double* Gl, int d, double thresh, double* R, int ldr,
+                           int* piv, double* sh) {
+  for (int t = threadIdx.x; t < d; t += NT) piv[t] = t;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  int k = 0;
+  for (; k < d; ++k) {
+    double bv = -1.0;
+    int bi = k;
+    for (int v = k + lane; v < d; v += 32) {
+      const int o = piv[v];
+      const double g = Gh[o + d * o];
+      if (g > bv) {
+        bv = g;
+        bi = v;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (!(bv > thresh)) break;  // uniform: every warp found the same maximum
+    __syncthreads();            // everyone has read piv
+    if (threadIdx.x == 0) {
+      const int q = piv[k];
+      piv[k] = piv[bi];
+      piv[bi] = q;
+      for (int r = 0; r < k; ++r) {  // earlier rows of R follow the column swap
+        const double a = R[r + ldr * k];
+        R[r + ldr * k] = R[r + ldr * bi];
+        R[r + ldr * bi] = a;
+      }
+      const int o = piv[k];
+      const double ah = Gh[o + d * o], al = Gl[o + d * o];
+      const double s = sqrt(ah);
+      const double p = s * s, pe = fma(s, s, -p);
+      const double r = ((ah - p) - pe + al) * (0.5 / s);
+      double sh_, sl_;
+      two_sum(s, r, sh_, sl_);
+      sh[0] = sh_;
+      sh[1] = sl_;
+      sh[2] = 1.0 / sh_;
+    }
+    __syncthreads();
+    const int pk = piv[k];
+    const double rh = sh[0], rl = sh[1], rinv = sh[2];
+    // row k: R_kj = G[pk, p_j] / r_kk, kept in G's row pk (dd)
+    for (int v = k + 1 + threadIdx.x; v < d; v += NT) {
+      const int o = piv[v];
+      const double ah = Gh[pk + d * o], al = Gl[pk + d * o];
+      const double q1 = ah * rinv;
+      double p, pe;
+      dd_mul(q1, 0.0, rh, rl, p, pe);
+      const double res = ((ah - p) - pe) + al;
+      const double q2 = res * rinv;
+      double qh, ql;
+      two_sum(q1, q2, qh, ql);
+      Gh[pk + d * o] = qh;
+      Gl[pk + d * o] = ql;
+      R[k + ldr * v] = qh + ql;
+    }
+    if (threadIdx.x == 0) R[k + ldr * k] = rh + rl;
+    __syncthreads();
+    // trailing update G[p_i, p_j] -= R_ki R_kj, i, j > k
+    const int m = d - k - 1;
+    for2d(m, m, [&](int a, int b) {
+      const int oi = piv[k + 1 + a], oj = piv[k + 1 + b];
+      double p, pe;
+      dd_mul(Gh[pk + d * oi], Gl[pk + d * oi], Gh[pk + d * oj], Gl[pk + d * oj], p, pe);
+      double s, e;
+      two_sum(Gh[oi + d * oj], -p, s, e);
+      double lo = Gl[oi + d * oj] + e - pe;
+      dd_norm(s, lo);
+      Gh[oi + d * oj] = s;
+      Gl[oi + d * oj] = lo;
+    });
+    __syncthreads();
+  }
+  return k;
+}
+
+// Singular values and leading left singular vectors of C from the factor R
+// (k x m, ld ldr, pivoted columns piv) with C C^T = Pi R^T R Pi^T: Jacobi
+// on X = R^T, U_C = Pi * normalised columns of X (svd_left without the QR).
+__device__ int svd_from_r(const double* R, int ldr, int k, int m, const int* piv,
+                          const SvdWork& w, double budget2, int cap, double* U, int ldu,
+                          double* margin_out, int* s_int) {
+  for2d(m, k, [&](int i, int r) { w.Xs[i + w.ldx * r] = i >= r ? R[r + ldr * i] : 0.0; });
+  __syncthreads();
+  const int sweeps = jacobi(w.Xs, w.ldx, m, k, w.vn);
+  if (w.prof && threadIdx.x == 0) {
+    atomicAdd(&w.prof[12], (unsigned long long)sweeps);
+    atomicAdd(&w.prof[13], 1ULL);
+    if (sweeps >= 60) atomicAdd(&w.prof[14], 1ULL);
+  }
+  for (int q = threadIdx.x; q < k; q += NT) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += w.Xs[i + w.ldx * q] * w.Xs[i + w.ldx * q];
+    w.sraw[q] = sqrt(s);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < k; q += NT) {
+    const double v = w.sraw[q];
+    int rank = 0;
+    for (int o = 0; o < k; ++o) {
+      const double u = w.sraw[o];
+      rank += (u > v) || (u == v && o < q);
+    }
+    w.sig[rank] = v;
+    w.perm[rank] = q;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *s_int = truncation_rank(w.sig, k, budget2, cap, margin_out);
+  __syncthreads();
+  const int t = *s_int;
+  for2d(m, t, [&](int i, int r) {
+    U[piv[i] + ldu * r] = w.Xs[i + w.ldx * w.perm[r]] / w.sig[r];
+  });
+  __syncthreads();
+  return t;
+}
+
+// Gram accumulation of the rows of T (rows x ncol, ld ldt) into the
+// register-resident upper-triangle entries (ei, ej) of this thread.
+template <int Q>
+__device__ __forceinline__ void gram_rows_acc(double (&gh)[Q], double (&gl)[Q], const int (&ei)[Q],
+                                              const int (&ej)[Q], const double* T, int ldt,
+                                              int ncol) {
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    if (ei[q] < 0) continue;
+    const double* a = T + ei[q];
+    const double* b = T + ej[q];
+    double h = gh[q], l = gl[q];
+    for (int c = 0; c < ncol; ++c) dd_fma_acc(h, l, a[ldt * c], b[ldt * c]);
+    gh[q] = h;
+    gl[q] = l;
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ void gram_store(double* Gh, double* Gl, int d, double (&gh)[Q],
+                                           double (&gl)[Q], const int (&ei)[Q], const int (&ej)[Q]) {
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    if (ei[q] < 0) continue;
+    double h = gh[q], l = gl[q];
+    dd_norm(h, l);
+    Gh[ei[q] + d * ej[q]] = h;
+    Gl[ei[q] + d * ej[q]] = l;
+    Gh[ej[q] + d * ei[q]] = h;
+    Gl[ej[q] + d * ei[q]] = l;
+  }
+}
+
 }  // namespace
 
 template <bool SMALL>
@@ -948,6 +1156,328 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
   __syncthreads();
   PROF(10);
 #undef PROF
+}
+
+// ---------------------------------------------------------------------------
+// Exact-Gram route (default): the two tall QRs of the TSQR route are
+// replaced by Gram matrices accumulated in double-double (every product
+// TwoProd-exact) and a pivoted double-double Cholesky, then the same
+// one-sided Jacobi on R^T.  The Gram of the FP64-computed slices is exact
+// to ~1e-32 relative, so sigma(R) carries the same ~u ||A|| absolute error
+// as the Householder R (rounding R to FP64) -- the rank decisions keep the
+// accuracy of the QR route -- while the slice loop has no sequential
+// column steps (3 barriers per slice instead of 2 per column).
+template <int Q>
+__global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
+  extern __shared__ double sm[];
+  const int n1 = p.n1, n2 = p.n2, n3 = p.n3;
+  const int mx = max(n1, n3);
+  const int RM1 = p.RM1, RM2 = p.RM2;
+  const int RMX = max(RM1, RM2);
+  const int ZR = max(2 * mx, RM2);
+  double* F = sm;                          // n1 x RMX   (cut 2 / output: X2)
+  double* lastT = F + n1 * RMX;            // n3 x RM2
+  double* tau = lastT + n3 * RM2;          // mx
+  double* Tb = tau + mx;                   // mx x mx    (slice block; V2 at the end)
+  double* G = Tb + mx * mx;                // ZR x mx    (Gram hi/lo planes; Z at the end)
+  double* Gl = G + mx * mx;
+  double* XP = G + ZR * mx;                // n1 x RMX   (cut 1: X; cut 2: P)
+  double* U1 = XP + n1 * RMX;              // n1 x n1
+  double* Xs = U1 + n1 * n1;               // mx x mx
+  double* Rc = Xs + mx * mx;               // mx x mx    (Cholesky factor)
+  double* Ms = Rc + mx * mx;               // p.MSMAX
+  double* sig = Ms + p.MSMAX;              // mx
+  double* sraw = sig + mx;                 // mx
+  double* vn = sraw + mx;                  // mx
+  double* sh = vn + mx;                    // 32 scalars
+  int* perm = reinterpret_cast<int*>(sh + 32);          // mx
+  int* piv = perm + mx;                                  // mx
+  int* colterm = piv + mx;                               // RM2
+  int* rowterm = colterm + RM2;                          // RM1
+  TermInfo* terms = reinterpret_cast<TermInfo*>(
+      reinterpret_cast<double*>(rowterm + RM1 + (((RM1 + RM2) & 1) ? 1 : 0)));
+  __shared__ int s_meta[8];
+
+  const int o = blockIdx.x;
+  if (o >= p.nout) return;
+  long long prof_t = p.prof ? clock64() : 0;
+#define PROF(k)                                                      \
+  if (p.prof && threadIdx.x == 0) {                                  \
+    const long long t_ = clock64();                                  \
+    atomicAdd(&p.prof[k], (unsigned long long)(t_ - prof_t));        \
+    prof_t = t_;                                                     \
+  }
+  const long long t0 = p.term_off ? p.term_off[o] : o;
+  const int K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
+
+  if (threadIdx.x == 0) {
+    int off1 = 0, off2 = 0, ms = 0;
+    for (int k = 0; k < K; ++k) {
+      const Term tm = p.terms[t0 + k];
+      const TSet& s = p.sets[tm.set];
+      TermInfo ti;
+      ti.r1 = s.ranks[2 * tm.idx];
+      ti.r2 = s.ranks[2 * tm.idx + 1];
+      ti.base = s.base + s.off[tm.idx];
+      double sc = tm.scale * s.uscale;
+      if (s.tscale) sc *= s.tscale[tm.idx];
+      ti.scale = sc;
+      ti.refl = tm.refl;
+      const double* fac = tm.fac >= 0 ? p.factors + (long long)tm.fac * (n1 + n2 + n3) : nullptr;
+      ti.u[0] = fac ? fac : nullptr;
+      ti.u[1] = fac ? fac + n1 : nullptr;
+      ti.u[2] = fac ? fac + n1 + n2 : nullptr;
+      ti.off1 = off1;
+      ti.off2 = off2;
+      ti.ms = ms;
+      off1 += ti.r1;
+      off2 += ti.r2;
+      ms += ti.r1 * ti.r2;
+      terms[k] = ti;
+    }
+    s_meta[0] = off1;
+    s_meta[1] = off2;
+  }
+  __syncthreads();
+  const int R1 = s_meta[0], R2 = s_meta[1];
+  for (int k = 0; k < K; ++k) {
+    const TermInfo& t = terms[k];
+    for (int a = threadIdx.x; a < t.r1; a += NT) rowterm[t.off1 + a] = k;
+    for (int b = threadIdx.x; b < t.r2; b += NT) colterm[t.off2 + b] = k;
+  }
+  for (int k = 0; k < K; ++k) {
+    const TermInfo& t = terms[k];
+    for2d(n1, t.r1, [&](int i, int a) {
+      const int ii = t.refl == 1 ? n1 - 1 - i : i;
+      double v = t.scale * t.base[ii + n1 * a];
+      if (t.u[0]) v *= t.u[0][i];
+      F[i + n1 * (t.off1 + a)] = v;
+    });
+    const double* L = t.base + (long long)n1 * t.r1 + (long long)n2 * t.r1 * t.r2;
+    for2d(t.r2, n3, [&](int b, int kk) {
+      const int kr = t.refl == 3 ? n3 - 1 - kk : kk;
+      double v = L[b + t.r2 * kr];
+      if (t.u[2]) v *= t.u[2][kk];
+      lastT[kk + n3 * (t.off2 + b)] = v;
+    });
+  }
+  __syncthreads();
+  PROF(0);
+  qr_inplace(lastT, n3, n3, R2, tau, sh);
+  const int q3 = min(n3, R2);
+  PROF(1);
+
+  // ---- cut 1: G1 = sum_j T_j T_j^T (n1 x n1), T_j = F M_j R3^T ----
+  int ei[Q], ej[Q];
+  double gh[Q], gl[Q];
+  {
+    const int ne = n1 * (n1 + 1) / 2;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int e = threadIdx.x + NT * q;
+      gh[q] = gl[q] = 0.0;
+      if (e < ne) tri_index(e, n1, ei[q], ej[q]);
+      else ei[q] = ej[q] = -1;
+    }
+  }
+  for (int j = 0; j < n2; ++j) {
+    __syncthreads();
+    stage_slice(Ms, terms, K, n1, n2, j);
+    __syncthreads();
+    left_times_blockdiag(XP, n1, F, n1, n1, R2, Ms, terms, colterm);
+    __syncthreads();
+    times_r3t(Tb, n1, false, XP, n1, n1, q3, R2, lastT, n3);
+    __syncthreads();
+    gram_rows_acc<Q>(gh, gl, ei, ej, Tb, n1, q3);
+  }
+  __syncthreads();
+  gram_store<Q>(G, Gl, n1, gh, gl, ei, ej);
+  __syncthreads();
+  PROF(2);
+  double loc = 0.0;
+  for (int i = threadIdx.x; i < n1; i += NT) loc += G[i + n1 * i] + Gl[i + n1 * i];
+  const double norm2 = block_sum(loc, sh + 8);
+  if (norm2 == 0.0 || !isfinite(norm2)) {
+    // canonical zero, TtTensor::constant(n1, n2, n3, 0) (reference :168)
+    if (threadIdx.x == 0) {
+      const long long sz = n1 + n2 + n3;
+      const unsigned long long at = atomicAdd(p.out.used, (unsigned long long)sz);
+      const bool ok = (long long)(at + sz) <= p.out.capacity;
+      if (!ok) atomicExch(&p.status[kStOverflow], 1);
+      if (!isfinite(norm2)) {
+        if (atomicCAS(&p.status[kStError], 0, kErrNonFinite) == 0) p.status[kStErrIdx] = o;
+      }
+      p.out.ranks[2 * o] = 1;
+      p.out.ranks[2 * o + 1] = 1;
+      p.out.off[o] = ok ? (long long)at : -1;
+      s_meta[2] = ok ? 1 : 0;
+      reinterpret_cast<long long*>(sh)[20] = (long long)at;
+      if (p.margins) {
+        p.margins[2 * o] = INFINITY;
+        p.margins[2 * o + 1] = INFINITY;
+      }
+    }
+    __syncthreads();
+    if (s_meta[2]) {
+      double* dst = p.out.base + reinterpret_cast<long long*>(sh)[20];
+      for (int e = threadIdx.x; e < n1 + n2 + n3; e += NT) dst[e] = e < n1 ? 0.0 : 1.0;
+    }
+    return;
+  }
+  const double budget2 = p.eps * p.eps * norm2 / 2.0;
+  const double cthresh = 1e-31 * norm2;
+  const SvdWork sw{p.prof, Xs, vn, sig, sraw, piv, perm, sh, mx};
+  const int k1 = chol_piv_dd(G, Gl, n1, cthresh, Rc, mx, piv, sh);
+  PROF(3);
+  double mg1 = 0.0;
+  const int t1 = svd_from_r(Rc, mx, k1, n1, piv, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
+  if (p.margins && threadIdx.x == 0) p.margins[2 * o] = mg1;
+  PROF(5);
+  for2d(t1, R1, [&](int r, int col) {  // P = U1^T F
+    double s = 0.0;
+    for (int i = 0; i < n1; ++i) s += U1[i + n1 * r] * F[i + n1 * col];
+    XP[r + n1 * col] = s;
+  });
+
+  // ---- cut 2: G2 = sum_j S_j^T S_j (q3 x q3), S_j = P M_j R3^T ----
+  double* X2 = F;
+  {
+    const int ne = q3 * (q3 + 1) / 2;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int e = threadIdx.x + NT * q;
+      gh[q] = gl[q] = 0.0;
+      if (e < ne) tri_index(e, q3, ei[q], ej[q]);
+      else ei[q] = ej[q] = -1;
+    }
+  }
+  for (int j = 0; j < n2; ++j) {
+    __syncthreads();
+    stage_slice(Ms, terms, K, n1, n2, j);
+    __syncthreads();
+    left_times_blockdiag(X2, n1, XP, n1, t1, R2, Ms, terms, colterm);
+    __syncthreads();
+    times_r3t(Tb, q3, true, X2, n1, t1, q3, R2, lastT, n3);  // S_j^T (q3 x t1)
+    __syncthreads();
+    gram_rows_acc<Q>(gh, gl, ei, ej, Tb, q3, t1);
+  }
+  __syncthreads();
+  gram_store<Q>(G, Gl, q3, gh, gl, ei, ej);
+  __syncthreads();
+  PROF(6);
+  const int k2 = chol_piv_dd(G, Gl, q3, cthresh, Rc, mx, piv, sh);
+  PROF(7);
+  double mg2 = 0.0;
+  double* W2 = Tb;  // V2 (q3 x t2), ld mx
+  const int t2 = svd_from_r(Rc, mx, k2, q3, piv, sw, budget2, p.cap, W2, mx, &mg2, &s_meta[5]);
+  PROF(9);
+  if (threadIdx.x == 0) {
+    if (p.margins) p.margins[2 * o + 1] = mg2;
+    const long long sz = (long long)n1 * t1 + (long long)n2 * t1 * t2 + (long long)t2 * n3;
+    const unsigned long long at = atomicAdd(p.out.used, (unsigned long long)sz);
+    const bool ok = (long long)(at + sz) <= p.out.capacity;
+    if (!ok) atomicExch(&p.status[kStOverflow], 1);
+    p.out.ranks[2 * o] = t1;
+    p.out.ranks[2 * o + 1] = t2;
+    p.out.off[o] = ok ? (long long)at : -1;
+    atomicMax(&p.status[kStMaxR1], t1);
+    atomicMax(&p.status[kStMaxR2], t2);
+    if (p.acc) {
+      double in_sz = 0.0;
+      for (int k = 0; k < K; ++k)
+        in_sz += (double)n1 * terms[k].r1 + (double)n2 * terms[k].r1 * terms[k].r2 +
+                 (double)terms[k].r2 * n3;
+      atomicAdd(&p.acc[0], round_flops((double)n2, (double)R1, (double)R2, (double)t1, (double)t2));
+      atomicAdd(&p.acc[1], 8.0 * (in_sz + (double)sz));
+    }
+    s_meta[2] = ok ? 1 : 0;
+    reinterpret_cast<long long*>(sh)[20] = (long long)at;
+  }
+  __syncthreads();
+  if (!s_meta[2]) return;
+  double* dst = p.out.base + reinterpret_cast<long long*>(sh)[20];
+  double* dmid = dst + (long long)n1 * t1;
+  double* dlast = dmid + (long long)n2 * t1 * t2;
+  for (int e = threadIdx.x; e < n1 * t1; e += NT) dst[e] = U1[e];
+  // G = [W2; 0] (n3 x t2) into Xs; Z = R3^T W2 (R2 x t2, ld ZR) into the Gram region
+  for2d(n3, t2, [&](int c, int s) { Xs[c + mx * s] = c < q3 ? W2[c + mx * s] : 0.0; });
+  double* Z = G;
+  for2d(R2, t2, [&](int b, int s) {
+    double acc = 0.0;
+    const int cm = min(b, q3 - 1);
+    for (int c = 0; c <= cm; ++c) acc += lastT[c + n3 * b] * W2[c + mx * s];
+    Z[b + ZR * s] = acc;
+  });
+  __syncthreads();
+  const int kmax = min(n3, R2);
+  for (int s = threadIdx.x; s < t2; s += NT) {
+    double* g = Xs + mx * s;
+    for (int k = kmax - 1; k >= 0; --k) {
+      const double t = tau[k];
+      if (t == 0.0) continue;
+      double w = g[k];
+      for (int i = k + 1; i < n3; ++i) w += lastT[i + n3 * k] * g[i];
+      w *= t;
+      g[k] -= w;
+      for (int i = k + 1; i < n3; ++i) g[i] -= w * lastT[i + n3 * k];
+    }
+  }
+  __syncthreads();
+  for2d(t2, n3, [&](int s, int kk) { dlast[s + t2 * kk] = Xs[kk + mx * s]; });
+  for (int j = 0; j < n2; ++j) {
+    __syncthreads();
+    stage_slice(Ms, terms, K, n1, n2, j);
+    __syncthreads();
+    left_times_blockdiag(X2, n1, XP, n1, t1, R2, Ms, terms, colterm);
+    __syncthreads();
+    for2d(t1, t2, [&](int r, int s) {
+      double a0 = 0.0, a1 = 0.0;
+      int b = 0;
+      for (; b + 1 < R2; b += 2) {
+        a0 += X2[r + n1 * b] * Z[b + ZR * s];
+        a1 += X2[r + n1 * (b + 1)] * Z[b + 1 + ZR * s];
+      }
+      if (b < R2) a0 += X2[r + n1 * b] * Z[b + ZR * s];
+      dmid[(long long)j * t1 * t2 + r + t1 * s] = a0 + a1;
+    });
+  }
+  __syncthreads();
+  PROF(10);
+#undef PROF
+}
+
+size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX) {
+  const size_t mx = n1 > n3 ? n1 : n3;
+  const size_t RMX = RM1 > RM2 ? RM1 : RM2;
+  const size_t ZR = (2 * mx > (size_t)RM2) ? 2 * mx : RM2;
+  size_t d = (size_t)n1 * RMX + (size_t)n3 * RM2 + mx + mx * mx + ZR * mx + (size_t)n1 * RMX +
+             (size_t)n1 * n1 + 2 * mx * mx + (size_t)MSMAX + 3 * mx + 32;
+  size_t ints = 2 * mx + RM2 + RM1 + 1;
+  return d * 8 + ((ints * 4 + 7) / 8) * 8 + sizeof(TermInfo) * kMaxTerms + 64;
+}
+
+cudaError_t launch_round_gram(const RoundArgs& a, cudaStream_t st) {
+  if (a.nout == 0) return cudaSuccess;
+  const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX);
+  const int mx = a.n1 > a.n3 ? a.n1 : a.n3;
+  const int ne = mx * (mx + 1) / 2;
+  cudaError_t e = cudaSuccess;
+#define LAUNCH_Q(QV)                                                                          \
+  e = cudaFuncSetAttribute(round_gram_kernel<QV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)smem);                                                         \
+  if (e != cudaSuccess) return e;                                                              \
+  round_gram_kernel<QV><<<a.nout, NT, smem, st>>>(a);
+  if (ne <= 3 * NT) {
+    LAUNCH_Q(3)
+  } else if (ne <= 5 * NT) {
+    LAUNCH_Q(5)
+  } else if (ne <= 10 * NT) {
+    LAUNCH_Q(10)
+  } else {
+    return cudaErrorInvalidValue;
+  }
+#undef LAUNCH_Q
+  return cudaGetLastError();
 }
 
 // Shared-memory bytes of the plan above.
