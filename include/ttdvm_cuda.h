@@ -144,6 +144,26 @@ int ttdvm_cuda_macro_batch(ttdvm_ctx* ctx, const ttdvm_tt_batch* in, double* out
 int ttdvm_cuda_collision_batch(ttdvm_ctx* ctx, const ttdvm_tt_batch* in, double eps,
                                double* macros);
 
+/* Face factors of oblique normals (replaces VelocityGrid::abs_xi_estimate /
+ * xi_normal_positive / xi_normal_negative, proj/src/velocity_grid.cpp:61-146):
+ * mode 0 = abs_xi_estimate(normal, cap), 1 = xi_normal_positive(normal,
+ * cap - 2) (i.e. from_full(max(xi_n,0), 1e-12, cap)), 2 = the negative part.
+ * normals [3*count] must be unit vectors.  Results go to the result batch
+ * (ttdvm_cuda_result_layout / _download).  diag (optional, 4 per normal):
+ * chosen candidate's squared Frobenius error, the runner-up's, the choice
+ * (2 * h index + strategy) and the smallest kept sigma^2 / sigma_max^2. */
+int ttdvm_cuda_face_factors(ttdvm_ctx* ctx, int32_t count, const double* normals, int32_t cap,
+                            int32_t mode, double* diag);
+
+/* Diffuse-wall ghost densities n_w of the last step (wall_ghost,
+ * proj/src/boundary.cpp:84-101), one per wall face in face order. */
+int ttdvm_cuda_wall_densities(ttdvm_ctx* ctx, double* out);
+
+/* Set-up facts of the last step's mesh: [0] distinct oblique normals,
+ * [1] of them with a kept singular value below 1e-12 sigma_max (FP64 Gram
+ * noise level), [2] wall faces, [3] face-factor build time (microseconds). */
+int ttdvm_cuda_setup_info(ttdvm_ctx* ctx, int64_t* info4);
+
 /* Device time (ms) of the kernels of the last call, by phase:
  * [0] moments, [1] shakhov build, [2] round f_S, [3] round collision,
  * [4] round fluxes, [5] round residual, [6] round update, [7] bookkeeping. */

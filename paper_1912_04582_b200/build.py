@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libttdvm_cuda.so")
-SOURCES = ["round.cu", "physics.cu", "capi.cu"]
+SOURCES = ["round.cu", "physics.cu", "facefactor.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr"]
@@ -26,20 +26,27 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    objs = []
-    for s in SOURCES:
+    objs, procs = [], []
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    headers.append(os.path.join(os.path.dirname(HERE), "include", "ttdvm_cuda.h"))
+    for s in SOURCES:  # the translation units compile in parallel
         o = os.path.join(CSRC, s.replace(".cu", ".o"))
+        objs.append(o)
+        if not force and os.path.exists(o) and all(
+                os.path.getmtime(d) <= os.path.getmtime(o)
+                for d in [os.path.join(CSRC, s), *headers] if os.path.exists(d)):
+            continue  # object newer than its source and every header
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
-        objs.append(o)
+        procs.append((subprocess.Popen(cmd), cmd))
+    for p, cmd in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
     subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
                     "-o", LIB + ".tmp"], check=True)
     os.replace(LIB + ".tmp", LIB)
-    for o in objs:
-        os.remove(o)
     return LIB
 
 

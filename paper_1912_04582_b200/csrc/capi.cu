@@ -17,6 +17,8 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <array>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/ttdvm_cuda.h"
@@ -43,6 +45,41 @@ cudaError_t launch_shakhov_raw(const double* macro, int count, int n, const doub
                                double R, double prandtl, double* out, cudaStream_t st);
 cudaError_t launch_gather(const TSet& s, int count, const long long* dst_off, int n1, int n2,
                           int n3, double* dst, cudaStream_t st);
+struct FaceFactorArgs {
+  int n;
+  const double* nodes;
+  int count;
+  const double* normals;
+  int cap;
+  int mode;
+  int* ranks;
+  double* cores;
+  long long stride;
+  double* diag;
+  int* status;
+};
+cudaError_t launch_face_factor(const FaceFactorArgs& a, cudaStream_t st);
+cudaError_t launch_xin(const double* normals, int count, int n, const double* nodes,
+                       double* cores, long long stride, int* ranks, cudaStream_t st);
+struct WallArgs {
+  int n;
+  int count;
+  const double* weights;
+  const int* face_of;
+  const int* pr;
+  const double* pcore;
+  const int* nrk;
+  const double* ncore;
+  long long fstride;
+  TSet state;
+  const int* cell;
+  const double* maxw;
+  double* denom;
+  double* nw;
+  int compute_denom;
+  int* status;
+};
+cudaError_t launch_wall(const WallArgs& a, cudaStream_t st);
 cudaError_t launch_dfma_probe(double* out, int blocks, int threads, int iters, cudaStream_t st);
 cudaError_t launch_place(const TSet& s, const int* src_ids, int count, int n1, int n2, int n3,
                          int* dst_ranks, long long* dst_off, const int* dst_ids,
@@ -128,7 +165,18 @@ long long tt_size(int n1, int n2, int n3, int r1, int r2) {
   return (long long)n1 * r1 + (long long)n2 * r1 * r2 + (long long)r2 * n3;
 }
 
-enum SetId { S_STATE = 0, S_FSRAW = 1, S_FS = 2, S_JR = 3, S_PHI = 4, S_RES = 5, S_FREE = 6, S_IN = 7 };
+enum SetId {
+  S_STATE = 0,
+  S_FSRAW = 1,
+  S_FS = 2,
+  S_JR = 3,
+  S_PHI = 4,
+  S_RES = 5,
+  S_FREE = 6,
+  S_IN = 7,
+  S_XIN = 8,   // exact rank-2 xi_n per oblique normal
+  S_EABS = 9,  // |xi_n| estimate per oblique normal
+};
 
 struct TermList {
   std::vector<long long> off;  // CSR
@@ -181,6 +229,19 @@ struct ttdvm_ctx {
   TensorSet state[2];
   int cur = 0;
   TensorSet fsraw, fs, jr, phi, res, freestream, in, result;
+  // oblique-normal face factors: per distinct
+  // normal, xi_n (exact rank 2) and the |xi_n| estimate E (rank <= cap_rank)
+  TensorSet xin, eabs;
+  std::vector<double> obl_normals;  // [3 * n_oblique]
+  int n_oblique = 0;
+  int imprecise = 0;
+  double ff_ms = 0.0;
+  // diffuse walls (T19): per wall face the xi_n^{+/-} factors, the unit
+  // Maxwellian M(1, T_w, 0), the setup denominator and the per-step n_w
+  int nwall = 0;
+  long long wstride = 0;
+  DevBuf<int> d_wface, d_wcell, d_wpr, d_wnr;
+  DevBuf<double> d_wpos, d_wneg, d_wmaxw, d_wden, d_nw;
   DevBuf<double> d_macro, d_nu;
   DevBuf<int> d_status;
   int* h_status = nullptr;  // pinned, kStWords + 2 longs
@@ -305,6 +366,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   a.term_off = tl.d_off.p;
   a.terms = tl.d_terms.p;
   a.factors = c->d_factors.p;
+  a.dscale = c->d_nw.p;
   a.n1 = a.n2 = a.n3 = n;
   a.nout = nout;
   a.eps = eps;
@@ -465,7 +527,8 @@ void run_collision(ttdvm_ctx* c, TensorSet& s, double eps, int count_ = -1) {
     c->t_fs.upload();
     c->t_col.upload();
   }
-  TensorSet* sets[kMaxSets] = {&s, &c->fsraw, &c->fs, &c->jr, &c->phi, &c->res, &c->freestream, &c->in};
+  TensorSet* sets[kMaxSets] = {&s,         &c->fsraw,      &c->fs, &c->jr,  &c->phi,
+                                &c->res,    &c->freestream, &c->in, &c->xin, &c->eabs};
   {
     Timer t(c, 2);
     run_round(c, c->t_fs, sets, c->fs, eps, 0, nullptr);
@@ -476,39 +539,280 @@ void run_collision(ttdvm_ctx* c, TensorSet& s, double eps, int count_ = -1) {
   }
 }
 
+// Exactly axis-aligned unit normal -> axis (0..2) and sign, else -1.
+int axis_of(const double* nv, double* sgn) {
+  int axis = -1;
+  for (int a = 0; a < 3; ++a) {
+    if (nv[a] != 0.0) {
+      if (axis >= 0) return -1;
+      axis = a;
+    }
+  }
+  if (axis >= 0 && sgn) *sgn = nv[axis];
+  return axis;
+}
+
+// Unit Maxwellian maxwell_tt(n, T, u) cores (proj/src/physics.cpp:69-87),
+// rank 1: [first n | middle n | last n], density folded into the first.
+void maxwell_cores(const ttdvm_ctx* c, double nd, double t, const double u[3], double* out) {
+  const int n = c->n;
+  const double two_rt = 2.0 * c->gas[1] * t;
+  const double norm1d = 1.0 / std::sqrt(M_PI * two_rt);
+  for (int a = 0; a < 3; ++a)
+    for (int i = 0; i < n; ++i) {
+      const double v = c->nodes[i] - u[a];
+      double val = norm1d * std::exp(-v * v / two_rt);
+      if (a == 0) val *= nd;
+      out[a * n + i] = val;
+    }
+}
+
+double elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
+  float f = 0.f;
+  cudaEventElapsedTime(&f, a, b);
+  return f;
+}
+
+// Face factors of the distinct oblique normals on the device: xi_n (exact
+// rank 2) and abs_xi_estimate(normal, 4) (velocity_grid.cpp:61-136).
+void build_oblique_factors(ttdvm_ctx* c) {
+  const int n = c->n, no = c->n_oblique;
+  ensure_static(c);
+  DevBuf<double> dn;
+  dn.alloc(std::max(1, 3 * no));
+  if (no) CK(cudaMemcpy(dn.p, c->obl_normals.data(), 24LL * no, cudaMemcpyHostToDevice));
+  const long long sx = 8LL * n;
+  c->xin.resize(no);
+  c->xin.arena.alloc(std::max<long long>(1, sx * no));
+  const int cap = 4;  // abs_flux_rank_cap, abs_xi_estimate(normal, 4)
+  const long long se = (long long)n * cap + (long long)n * cap * cap + (long long)cap * n;
+  c->eabs.resize(no);
+  c->eabs.arena.alloc(std::max<long long>(1, se * no));
+  std::vector<long long> of(std::max(1, no));
+  for (int i = 0; i < no; ++i) of[i] = i * sx;
+  if (no) CK(cudaMemcpy(c->xin.off.p, of.data(), 8LL * no, cudaMemcpyHostToDevice));
+  for (int i = 0; i < no; ++i) of[i] = i * se;
+  if (no) CK(cudaMemcpy(c->eabs.off.p, of.data(), 8LL * no, cudaMemcpyHostToDevice));
+  CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
+  CK(cudaEventRecord(c->ev0, c->st));
+  CK(launch_xin(dn.p, no, n, c->d_nodes.p, c->xin.arena.p, sx, c->xin.ranks.p, c->st));
+  FaceFactorArgs a;
+  a.n = n;
+  a.nodes = c->d_nodes.p;
+  a.count = no;
+  a.normals = dn.p;
+  a.cap = cap;
+  a.mode = 0;
+  a.ranks = c->eabs.ranks.p;
+  a.cores = c->eabs.arena.p;
+  a.stride = se;
+  a.diag = nullptr;
+  a.status = c->d_status.p;
+  CK(launch_face_factor(a, c->st));
+  CK(cudaEventRecord(c->ev1, c->st));
+  c->launches += 2;
+  CK(cudaMemcpyAsync(c->h_status, c->d_status.p, kStWords * sizeof(int), cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->ff_ms = elapsed_ms(c->ev0, c->ev1);
+  if (c->h_status[kStError])
+    throw Fail{TTDVM_EDOMAIN, "abs_xi_estimate: degenerate operand for oblique normal " +
+                                  std::to_string(c->h_status[kStErrIdx])};
+  c->imprecise = c->h_status[kStAux];
+  c->xin.used = sx * no;
+  c->xin.maxr1 = c->xin.maxr2 = 2;
+  c->eabs.used = se * no;
+  c->eabs.maxr1 = c->eabs.maxr2 = cap;
+  dn.free();
+}
+
+// Diffuse-wall faces: xi_n^{+/-} = from_full(max/min(xi_n, 0), 1e-12, cap + 2)
+// (velocity_grid.cpp:127-128; analytic rank 1 for axis-aligned normals,
+// where the reference's SVD gives the same rank-1 tensor), the unit wall
+// Maxwellian and the state-independent denominator of n_w.
+void build_walls(ttdvm_ctx* c, const std::vector<int>& wall_faces) {
+  const int n = c->n, nw = (int)wall_faces.size();
+  c->nwall = nw;
+  if (nw == 0) return;
+  const int cap = 6;  // cap_rank + 2 (wall_ghost(..., 4), boundary.cpp:86-87)
+  const long long st = (long long)n * cap + (long long)n * cap * cap + (long long)cap * n;
+  c->wstride = st;
+  c->d_wpos.alloc(st * nw);
+  c->d_wneg.alloc(st * nw);
+  c->d_wpr.alloc(2 * nw);
+  c->d_wnr.alloc(2 * nw);
+  c->d_wface.alloc(nw);
+  c->d_wcell.alloc(nw);
+  c->d_wmaxw.alloc(3LL * n * nw);
+  c->d_wden.alloc(nw);
+  c->d_nw.alloc(nw);
+  std::vector<double> obl, mw(3LL * n * nw);
+  std::vector<int> obl_w, cells(nw);
+  for (int w = 0; w < nw; ++w) {
+    const int f = wall_faces[w];
+    cells[w] = c->left[f];
+    const ttdvm_bc& b = c->bcs[c->group[f]];
+    const double u0[3] = {0.0, 0.0, 0.0};
+    maxwell_cores(c, 1.0, b.wall_temperature, u0, &mw[3LL * n * w]);
+    const double* nv = &c->normal[3 * f];
+    double sgn = 0.0;
+    const int axis = axis_of(nv, &sgn);
+    if (axis < 0) {
+      obl.insert(obl.end(), nv, nv + 3);
+      obl_w.push_back(w);
+      continue;
+    }
+    for (int pm = 0; pm < 2; ++pm) {
+      std::vector<double> core(3 * n, 1.0);
+      for (int i = 0; i < n; ++i) {
+        const double v = sgn * c->nodes[i];
+        core[axis * n + i] = pm == 0 ? (v > 0.0 ? v : 0.0) : (v < 0.0 ? v : 0.0);
+      }
+      const int rk[2] = {1, 1};
+      CK(cudaMemcpy((pm == 0 ? c->d_wpos.p : c->d_wneg.p) + st * w, core.data(), 24LL * n,
+                    cudaMemcpyHostToDevice));
+      CK(cudaMemcpy((pm == 0 ? c->d_wpr.p : c->d_wnr.p) + 2 * w, rk, 8, cudaMemcpyHostToDevice));
+    }
+  }
+  CK(cudaMemcpy(c->d_wface.p, wall_faces.data(), 4LL * nw, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_wcell.p, cells.data(), 4LL * nw, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_wmaxw.p, mw.data(), 8LL * mw.size(), cudaMemcpyHostToDevice));
+  const int no = (int)obl_w.size();
+  if (no) {
+    DevBuf<double> dn, tp, tn;
+    DevBuf<int> rp, rn;
+    dn.alloc(3 * no);
+    tp.alloc(st * no);
+    tn.alloc(st * no);
+    rp.alloc(2 * no);
+    rn.alloc(2 * no);
+    CK(cudaMemcpy(dn.p, obl.data(), 24LL * no, cudaMemcpyHostToDevice));
+    CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
+    for (int pm = 0; pm < 2; ++pm) {
+      FaceFactorArgs a;
+      a.n = n;
+      a.nodes = c->d_nodes.p;
+      a.count = no;
+      a.normals = dn.p;
+      a.cap = cap;
+      a.mode = 1 + pm;
+      a.ranks = pm == 0 ? rp.p : rn.p;
+      a.cores = pm == 0 ? tp.p : tn.p;
+      a.stride = st;
+      a.diag = nullptr;
+      a.status = c->d_status.p;
+      CK(launch_face_factor(a, c->st));
+      c->launches += 1;
+    }
+    for (int i = 0; i < no; ++i) {
+      const int w = obl_w[i];
+      CK(cudaMemcpyAsync(c->d_wpos.p + st * w, tp.p + st * i, 8LL * st, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(c->d_wneg.p + st * w, tn.p + st * i, 8LL * st, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(c->d_wpr.p + 2 * w, rp.p + 2 * i, 8, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(c->d_wnr.p + 2 * w, rn.p + 2 * i, 8, cudaMemcpyDeviceToDevice, c->st));
+    }
+    CK(cudaMemcpyAsync(c->h_status, c->d_status.p, kStWords * sizeof(int), cudaMemcpyDeviceToHost,
+                       c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (c->h_status[kStError])
+      throw Fail{TTDVM_EDOMAIN, "xi_normal_positive/negative: degenerate wall normal"};
+    dn.free();
+    tp.free();
+    tn.free();
+    rp.free();
+    rn.free();
+  }
+}
+
+WallArgs wall_args(ttdvm_ctx* c, const TensorSet& s, int compute_denom) {
+  WallArgs a;
+  a.n = c->n;
+  a.count = c->nwall;
+  a.weights = c->d_weights.p;
+  a.face_of = c->d_wface.p;
+  a.pr = c->d_wpr.p;
+  a.pcore = c->d_wpos.p;
+  a.nrk = c->d_wnr.p;
+  a.ncore = c->d_wneg.p;
+  a.fstride = c->wstride;
+  a.state = s.view();
+  a.cell = c->d_wcell.p;
+  a.maxw = c->d_wmaxw.p;
+  a.denom = c->d_wden.p;
+  a.nw = c->d_nw.p;
+  a.compute_denom = compute_denom;
+  a.status = c->d_status.p;
+  return a;
+}
+
+// n_w per wall face from the current state (wall_ghost, boundary.cpp:84-101).
+void run_walls(ttdvm_ctx* c, const TensorSet& s, int compute_denom) {
+  if (c->nwall == 0) return;
+  ensure_static(c);
+  CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
+  CK(launch_wall(wall_args(c, s, compute_denom), c->st));
+  c->launches += 1;
+  CK(cudaMemcpyAsync(c->h_status, c->d_status.p, kStWords * sizeof(int), cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (c->h_status[kStError] == kErrWallDegenerate)
+    throw Fail{TTDVM_EDOMAIN, "wall_ghost: degenerate wall Maxwellian flux (face " +
+                                  std::to_string(c->h_status[kStErrIdx]) + ")"};
+  if (c->h_status[kStError] == kErrWallDensity)
+    throw Fail{TTDVM_EDOMAIN,
+               "wall_ghost: impermeability balance gave nonpositive density (face " +
+                   std::to_string(c->h_status[kStErrIdx]) + ")"};
+}
+
 // Static summand lists of the step (rebuilt when mesh / BCs / grid change).
 void build_step_terms(ttdvm_ctx* c) {
   if (!c->terms_dirty) return;
   require(c->n > 0, "set_grid first");
   require(c->ncell > 0, "set_mesh first");
   const int n = c->n;
-  // face factors (xi.n)^{+/-} for axis-aligned normals: exactly
-  // ((xi_n +- |xi_n|)/2) on one axis, ones on the others (SURVEY.md §8(a)
-  // T13; the reference's rank-1 E for axis normals is exact,
-  // proj/tests/test_velocity_grid.cpp:98-115).
+  const int ng = (int)c->bcs.size();
+  // ---- face factors ----
+  // axis-aligned normals: (xi.n)^{+/-} = ((xi_n +- |xi_n|)/2) on one axis and
+  // ones on the others, exactly the reference's (its rank-1 E is exact for
+  // axis normals, proj/tests/test_velocity_grid.cpp:98-115); oblique
+  // normals: xi_n and E per distinct normal, computed on the device.
   c->factors.clear();
-  std::vector<int> facp(c->nface), facm(c->nface);
-  std::vector<int> key_of;  // (axis*2 + sign) -> factor pair id
+  std::vector<int> facp(c->nface, -1), facm(c->nface, -1), nid(c->nface, -1);
   int pair_id[6];
   for (int k = 0; k < 6; ++k) pair_id[k] = -1;
+  struct KeyHash {
+    size_t operator()(const std::array<long long, 3>& k) const {
+      return std::hash<long long>()(k[0] * 1000003LL ^ k[1] * 7919LL ^ k[2]);
+    }
+  };
+  std::unordered_map<std::array<long long, 3>, int, KeyHash> key_of;
+  c->obl_normals.clear();
   for (int f = 0; f < c->nface; ++f) {
     const double* nv = &c->normal[3 * f];
-    int axis = -1;
+    const double nn = std::sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+    require(std::fabs(nn - 1.0) <= 1e-12, "xi_normal: normal must be a unit vector (face " +
+                                              std::to_string(f) + ")");
     double sgn = 0.0;
-    for (int a = 0; a < 3; ++a) {
-      if (nv[a] != 0.0) {
-        if (axis >= 0) axis = 9;
-        else axis = a;
+    const int axis = axis_of(nv, &sgn);
+    if (axis < 0) {
+      // VelocityGrid::cached key: normal quantised to 1e-12 (velocity_grid.cpp:66-69)
+      const std::array<long long, 3> key = {std::llround(nv[0] / 1e-12),
+                                            std::llround(nv[1] / 1e-12),
+                                            std::llround(nv[2] / 1e-12)};
+      auto it = key_of.find(key);
+      if (it == key_of.end()) {
+        const int id = (int)(c->obl_normals.size() / 3);
+        key_of.emplace(key, id);
+        c->obl_normals.insert(c->obl_normals.end(), nv, nv + 3);
+        nid[f] = id;
+      } else {
+        nid[f] = it->second;
       }
+      continue;
     }
-    require(axis >= 0 && axis < 3,
-            "face " + std::to_string(f) +
-                ": oblique normals need the general face-factor builder (SURVEY.md §8(f) N1)");
-    sgn = nv[axis];
-    require(std::fabs(std::fabs(sgn) - 1.0) <= 1e-12, "xi_normal: normal must be a unit vector");
     const int key = axis * 2 + (sgn > 0 ? 1 : 0);
     if (pair_id[key] < 0) {
-      pair_id[key] = (int)(c->factors.size() / (3 * n)) ;
+      pair_id[key] = (int)(c->factors.size() / (3 * n));
       for (int pm = 0; pm < 2; ++pm) {
         std::vector<double> fac(3 * n, 1.0);
         for (int i = 0; i < n; ++i) {
@@ -522,12 +826,16 @@ void build_step_terms(ttdvm_ctx* c) {
     facp[f] = pair_id[key];
     facm[f] = pair_id[key] + 1;
   }
+  c->n_oblique = (int)(c->obl_normals.size() / 3);
+  if (c->n_oblique > 0)
+    require(n <= 48, "oblique face normals need a velocity grid of at most 48 nodes per axis");
   c->d_factors.alloc(std::max<size_t>(1, c->factors.size()));
   if (!c->factors.empty())
     CK(cudaMemcpy(c->d_factors.p, c->factors.data(), c->factors.size() * 8, cudaMemcpyHostToDevice));
+  build_oblique_factors(c);
 
-  // freestream Maxwellians per group (maxwell_tt, proj/src/physics.cpp:69-87)
-  const int ng = (int)c->bcs.size();
+  // ---- free-stream Maxwellians per group (maxwell_tt, physics.cpp:69-87);
+  // wall groups hold the unit wall Maxwellian M(1, T_w, 0) ----
   {
     std::vector<int> rk(2 * std::max(1, ng), 1);
     std::vector<long long> of(std::max(1, ng));
@@ -537,15 +845,10 @@ void build_step_terms(ttdvm_ctx* c) {
       const ttdvm_bc& b = c->bcs[g];
       if (b.kind == 4 || b.kind == 5) {
         require(b.free_n > 0.0 && b.free_t > 0.0, "maxwell_tt: state must have n > 0, T > 0");
-        const double two_rt = 2.0 * c->gas[1] * b.free_t;
-        const double norm1d = 1.0 / std::sqrt(M_PI * two_rt);
-        for (int a = 0; a < 3; ++a)
-          for (int i = 0; i < n; ++i) {
-            const double v = c->nodes[i] - b.free_u[a];
-            double val = norm1d * std::exp(-v * v / two_rt);
-            if (a == 0) val *= b.free_n;
-            cores[(size_t)g * 3 * n + a * n + i] = val;
-          }
+        maxwell_cores(c, b.free_n, b.free_t, b.free_u, &cores[(size_t)g * 3 * n]);
+      } else if (b.kind == 0) {
+        const double u0[3] = {0.0, 0.0, 0.0};
+        maxwell_cores(c, 1.0, b.wall_temperature, u0, &cores[(size_t)g * 3 * n]);
       }
     }
     c->freestream.resize(std::max(1, ng));
@@ -556,26 +859,63 @@ void build_step_terms(ttdvm_ctx* c) {
     c->freestream.maxr1 = c->freestream.maxr2 = 1;
   }
 
-  // flux: Phi_f = round(xp o f_L + xm o f_R)
+  // ---- walls ----
+  std::vector<int> wall_faces, wall_of(c->nface, -1);
+  for (int f = 0; f < c->nface; ++f) {
+    if (c->right[f] >= 0) continue;
+    const int g = c->group[f];
+    require(g >= 0 && g < ng, "boundary face " + std::to_string(f) + " has no boundary condition");
+    if (c->bcs[g].kind == 0) {
+      wall_of[f] = (int)wall_faces.size();
+      wall_faces.push_back(f);
+    }
+  }
+  build_walls(c, wall_faces);
+  run_walls(c, c->state[c->cur], 1);  // state-independent denominators
+
+  // ---- flux: Phi_f = round(xp o f_L + xm o f_R) ----
+  // oblique normals: xp = (xi_n + E)/2, xm = (xi_n - E)/2 enter as the four
+  // Hadamard terms 0.5 xi_n o f_L, 0.5 E o f_L, 0.5 xi_n o f_R, -0.5 E o f_R
+  // (the reference rounds xp, xm at 1e-14 first -- the same tensors to 1e-14)
   TermList& fl = c->t_flux;
   fl.off.assign(1, 0);
   fl.terms.clear();
+  fl.terms.reserve((size_t)c->nface * 4);
   for (int f = 0; f < c->nface; ++f) {
-    fl.terms.push_back(Term{S_STATE, c->left[f], 1.0, facp[f], 0});
+    Term L{S_STATE, c->left[f], 1.0}, R{S_STATE, 0, 1.0};
     const int r = c->right[f];
     if (r >= 0) {
-      fl.terms.push_back(Term{S_STATE, r, 1.0, facm[f], 0});
+      R.idx = r;
     } else {
       const int g = c->group[f];
-      require(g >= 0 && g < ng, "boundary face " + std::to_string(f) + " has no boundary condition");
       const int kind = c->bcs[g].kind;
       if (kind >= 1 && kind <= 3) {
-        fl.terms.push_back(Term{S_STATE, c->left[f], 1.0, facm[f], kind});
+        R.idx = c->left[f];  // symmetry_ghost: mode reflection (boundary.cpp:103-107)
+        R.refl = kind;
       } else if (kind == 4 || kind == 5) {
-        fl.terms.push_back(Term{S_FREE, g, 1.0, facm[f], 0});
+        R.set = S_FREE;      // freestream_ghost (boundary.hpp:51-53)
+        R.idx = g;
       } else {
-        throw Fail{TTDVM_EINVAL,
-                   "wall boundaries need the wall-ghost kernel (SURVEY.md §8(f) N3)"};
+        R.set = S_FREE;      // wall_ghost = n_w M(1, T_w, 0) (boundary.cpp:84-101)
+        R.idx = g;
+        R.dsi = wall_of[f];
+      }
+    }
+    if (nid[f] < 0) {
+      L.fac = facp[f];
+      R.fac = facm[f];
+      fl.terms.push_back(L);
+      fl.terms.push_back(R);
+    } else {
+      for (int side = 0; side < 2; ++side) {
+        Term t = side == 0 ? L : R;
+        t.fidx = nid[f];
+        t.fset = S_XIN;
+        t.scale = 0.5;
+        fl.terms.push_back(t);
+        t.fset = S_EABS;
+        t.scale = side == 0 ? 0.5 : -0.5;
+        fl.terms.push_back(t);
       }
     }
     fl.off.push_back((long long)fl.terms.size());
@@ -662,9 +1002,11 @@ void step_once(ttdvm_ctx* c, double dt, double eps, int cap) {
   // rounding, physics.cpp:118)
   run_collision(c, s, eps, nown);
   c->jr.tscale = c->d_nu.p;
-  TensorSet* sets[kMaxSets] = {&s, &c->fsraw, &c->fs, &c->jr, &c->phi, &c->res, &c->freestream, &c->in};
+  TensorSet* sets[kMaxSets] = {&s,         &c->fsraw,      &c->fs, &c->jr,  &c->phi,
+                                &c->res,    &c->freestream, &c->in, &c->xin, &c->eabs};
   {
     Timer t(c, 4);
+    run_walls(c, s, 0);
     run_round(c, c->t_flux, sets, c->phi, eps, cap, nullptr);
   }
   c->res.uscale = 1.0;
@@ -755,12 +1097,14 @@ int ttdvm_cuda_destroy(ttdvm_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   for (TensorSet* s : {&c->state[0], &c->state[1], &c->fsraw, &c->fs, &c->jr, &c->phi, &c->res,
-                       &c->freestream, &c->in, &c->result})
+                       &c->freestream, &c->in, &c->result, &c->xin, &c->eabs})
     s->free();
   for (TermList* t : {&c->t_fs, &c->t_col, &c->t_flux, &c->t_res, &c->t_upd, &c->t_batch}) t->free();
   c->d_nodes.free();
   c->d_weights.free();
   c->d_factors.free();
+  for (DevBuf<int>* b : {&c->d_wface, &c->d_wcell, &c->d_wpr, &c->d_wnr}) b->free();
+  for (DevBuf<double>* b : {&c->d_wpos, &c->d_wneg, &c->d_wmaxw, &c->d_wden, &c->d_nw}) b->free();
   c->d_macro.free();
   c->d_nu.free();
   c->d_status.free();
@@ -988,6 +1332,79 @@ int ttdvm_cuda_collision_batch(ttdvm_ctx* c, const ttdvm_tt_batch* in, double ep
     c->t_fs.off.clear();
     if (macros && c->in.count)
       CK(cudaMemcpy(macros, c->d_macro.p, 88LL * c->in.count, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ttdvm_cuda_face_factors(ttdvm_ctx* c, int32_t count, const double* normals, int32_t cap,
+                            int32_t mode, double* diag) {
+  return guard(c, [&] {
+    require(c->n > 0, "set_grid first");
+    require(c->n <= 48, "face factors need a velocity grid of at most 48 nodes per axis");
+    require(count >= 0 && (count == 0 || normals), "null normals");
+    require(cap >= 1 && cap <= 8, "normal tensors: cap_rank >= 1");
+    require(mode >= 0 && mode <= 2, "unknown face factor mode");
+    for (int i = 0; i < count; ++i) {
+      const double* nv = normals + 3 * i;
+      require(std::fabs(std::sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]) - 1.0) <= 1e-12,
+              "normal tensors: normal must be a unit vector");
+    }
+    cudaSetDevice(c->device);
+    ensure_static(c);
+    const int n = c->n;
+    const long long st = (long long)n * cap + (long long)n * cap * cap + (long long)cap * n;
+    DevBuf<double> dn, dd;
+    dn.alloc(std::max(1, 3 * count));
+    if (count) CK(cudaMemcpy(dn.p, normals, 24LL * count, cudaMemcpyHostToDevice));
+    if (diag) dd.alloc(std::max(1, 4 * count));
+    c->result.free();
+    c->result.resize(count);
+    c->result.arena.alloc(std::max<long long>(1, st * count));
+    std::vector<long long> of(std::max(1, count));
+    for (int i = 0; i < count; ++i) of[i] = i * st;
+    if (count) CK(cudaMemcpy(c->result.off.p, of.data(), 8LL * count, cudaMemcpyHostToDevice));
+    CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
+    FaceFactorArgs a;
+    a.n = n;
+    a.nodes = c->d_nodes.p;
+    a.count = count;
+    a.normals = dn.p;
+    a.cap = cap;
+    a.mode = mode;
+    a.ranks = c->result.ranks.p;
+    a.cores = c->result.arena.p;
+    a.stride = st;
+    a.diag = diag ? dd.p : nullptr;
+    a.status = c->d_status.p;
+    c->launches = 0;
+    CK(launch_face_factor(a, c->st));
+    c->launches += 1;
+    CK(cudaMemcpyAsync(c->h_status, c->d_status.p, kStWords * sizeof(int), cudaMemcpyDeviceToHost,
+                       c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (c->h_status[kStError])
+      throw Fail{TTDVM_EDOMAIN, "normal tensors: degenerate operand for normal " +
+                                    std::to_string(c->h_status[kStErrIdx])};
+    c->imprecise = c->h_status[kStAux];
+    c->result.used = st * count;
+    c->result.maxr1 = c->result.maxr2 = cap;
+    if (diag && count) CK(cudaMemcpy(diag, dd.p, 32LL * count, cudaMemcpyDeviceToHost));
+    dn.free();
+    dd.free();
+  });
+}
+
+int ttdvm_cuda_wall_densities(ttdvm_ctx* c, double* out) {
+  return guard(c, [&] {
+    if (c->nwall) CK(cudaMemcpy(out, c->d_nw.p, 8LL * c->nwall, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ttdvm_cuda_setup_info(ttdvm_ctx* c, int64_t* info4) {
+  return guard(c, [&] {
+    info4[0] = c->n_oblique;
+    info4[1] = c->imprecise;
+    info4[2] = c->nwall;
+    info4[3] = (int64_t)(c->ff_ms * 1000.0);
   });
 }
 

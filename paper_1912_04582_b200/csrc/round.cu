@@ -29,116 +29,117 @@
 // reference keeps Sigma_2 in last, here it sits in middle).
 #include <math.h>
 
-#include "ttdvm_device.cuh"
+#include "linalg.cuh"
 
 namespace ttdvm {
 
 namespace {
 
-constexpr int NT = kRoundThreads;
-constexpr int NW = NT / 32;
 
 struct TermInfo {
-  const double* base;
-  const double* u[3];
+  const double* base;   // state-like operand (ranks b1, b2)
+  const double* fb;     // Hadamard TT factor (ranks fa1, fa2) or null
+  const double* u[3];   // rank-1 face factor (axis-aligned normals) or null
   double scale;
   int r1, r2, off1, off2, refl, ms;
+  int b1, b2, fa1, fa2;
 };
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-template <int W>
-__device__ __forceinline__ double group_sum(double v) {
-#pragma unroll
-  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-__device__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  double s = 0.0;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) s += red[w];
-  return s;
-}
-
-// FP64 reciprocal and reciprocal square root with an FP32 seed and two
-// Newton steps in FP64 (23 -> 46 -> 92 bits, i.e. correct to a few ulps):
-// the IEEE-exact double div/sqrt sequences sit on the serial critical path
-// of every Householder and Jacobi step.  Exponents are split off exactly so
-// the FP32 seed never over- or underflows.
-__device__ __forceinline__ double fast_rcp(double x) {
-  const long long bits = __double_as_longlong(x);
-  const int e = (int)((bits >> 52) & 0x7ff) - 1023;
-  const double m = __longlong_as_double((bits & ~(0x7ffLL << 52)) | (1023LL << 52));  // [1,2)
-  double r = (double)__frcp_rn((float)m);
-  r = r * (2.0 - m * r);
-  r = r * (2.0 - m * r);
-  return r * __longlong_as_double((long long)(1023 - e) << 52);
-}
-
-__device__ __forceinline__ double fast_rsqrt(double x) {  // x > 0, normal
-  const long long bits = __double_as_longlong(x);
-  int e = (int)((bits >> 52) & 0x7ff) - 1023;
-  const int odd = e & 1;
-  e -= odd;  // even exponent: x = m * 2^e, m in [1, 4)
-  const double m = __longlong_as_double((bits & ~(0x7ffLL << 52)) | ((long long)(1023 + odd) << 52));
-  double r = (double)rsqrtf((float)m);
-  r = r * (1.5 - 0.5 * m * r * r);
-  r = r * (1.5 - 0.5 * m * r * r);
-  return r * __longlong_as_double((long long)(1023 - e / 2) << 52);
-}
-
-// LAPACK dlarfg on (alpha, ||x||^2): H = I - tau v v^T, v = [1; x*scale],
-// tau = (beta - alpha)/beta = 1 - alpha/beta, with 1/|beta| from one rsqrt.
-__device__ __forceinline__ void larfg(double alpha, double sigma2, double& beta, double& tau,
-                                      double& scale) {
-  if (sigma2 == 0.0) {
-    beta = alpha;
-    tau = 0.0;
-    scale = 0.0;
-    return;
+// Resolve the summands of output o into TermInfo (thread 0) and the row /
+// column -> term maps.  A term's ranks are (fa1 b1, fa2 b2): the Hadamard
+// product fb o base (proj/src/tt_tensor.cpp:212-245) is never formed, its
+// Kronecker-structured cores are built on the fly where they are consumed.
+__device__ void setup_terms(const RoundArgs& p, int o, TermInfo* terms, int* rowterm,
+                            int* colterm, int* s_meta, int& K, int& R1, int& R2) {
+  const long long t0 = p.term_off ? p.term_off[o] : (long long)o;
+  K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
+  const int n1 = p.n1, n2 = p.n2, n3 = p.n3;
+  if (threadIdx.x == 0) {
+    int off1 = 0, off2 = 0, ms = 0;
+    for (int k = 0; k < K; ++k) {
+      const Term tm = p.terms[t0 + k];
+      const TSet& s = p.sets[tm.set];
+      TermInfo ti;
+      ti.b1 = s.ranks[2 * tm.idx];
+      ti.b2 = s.ranks[2 * tm.idx + 1];
+      ti.base = s.base + s.off[tm.idx];
+      double sc = tm.scale * s.uscale;
+      if (s.tscale) sc *= s.tscale[tm.idx];
+      if (tm.dsi >= 0) sc *= p.dscale[tm.dsi];
+      ti.scale = sc;
+      ti.refl = tm.refl;
+      const double* fac = tm.fac >= 0 ? p.factors + (long long)tm.fac * (n1 + n2 + n3) : nullptr;
+      ti.u[0] = fac ? fac : nullptr;
+      ti.u[1] = fac ? fac + n1 : nullptr;
+      ti.u[2] = fac ? fac + n1 + n2 : nullptr;
+      if (tm.fset >= 0) {
+        const TSet& f = p.sets[tm.fset];
+        ti.fa1 = f.ranks[2 * tm.fidx];
+        ti.fa2 = f.ranks[2 * tm.fidx + 1];
+        ti.fb = f.base + f.off[tm.fidx];
+      } else {
+        ti.fa1 = ti.fa2 = 1;
+        ti.fb = nullptr;
+      }
+      ti.r1 = ti.fa1 * ti.b1;
+      ti.r2 = ti.fa2 * ti.b2;
+      ti.off1 = off1;
+      ti.off2 = off2;
+      ti.ms = ms;
+      off1 += ti.r1;
+      off2 += ti.r2;
+      ms += ti.r1 * ti.r2;
+      terms[k] = ti;
+    }
+    s_meta[0] = off1;
+    s_meta[1] = off2;
   }
-  const double h = alpha * alpha + sigma2;
-  const double ri = fast_rsqrt(h);
-  const double nrm = h * ri;
-  beta = alpha >= 0.0 ? -nrm : nrm;
-  const double rb = alpha >= 0.0 ? -ri : ri;  // 1 / beta
-  tau = 1.0 - alpha * rb;
-  scale = fast_rcp(alpha - beta);
-}
-
-// Visit (r, c) in [0, rows) x [0, cols) without integer division: threads
-// are split into power-of-two row lanes (r = tid & (rp - 1)) and column
-// strides.  No barriers or shuffles may be used inside f.
-template <class Fn>
-__device__ __forceinline__ void for2d(int rows, int cols, Fn&& f) {
-  if (rows <= 0 || cols <= 0) return;
-  const int lg = rows <= 1 ? 0 : 32 - __clz(rows - 1);
-  if ((1 << lg) <= NT) {
-    const int r = threadIdx.x & ((1 << lg) - 1);
-    if (r >= rows) return;
-    const int step = NT >> lg;
-    for (int c = threadIdx.x >> lg; c < cols; c += step) f(r, c);
-  } else {
-    for (int r = threadIdx.x; r < rows; r += NT)
-      for (int c = 0; c < cols; ++c) f(r, c);
+  __syncthreads();
+  R1 = s_meta[0];
+  R2 = s_meta[1];
+  for (int k = 0; k < K; ++k) {
+    const TermInfo& t = terms[k];
+    for (int a = threadIdx.x; a < t.r1; a += NT) rowterm[t.off1 + a] = k;
+    for (int b = threadIdx.x; b < t.r2; b += NT) colterm[t.off2 + b] = k;
   }
 }
 
-__device__ __forceinline__ int floor_pow2(int x) {
-  int p = 1;
-  while (p * 2 <= x) p *= 2;
-  return p;
+// F (n1 x R1, ld n1) and last^T (n3 x R2, ld n3) of the implicit sum.
+// Hadamard column order follows the reference: (p, q) -> p * b + q.
+__device__ void materialise_outer(double* F, double* lastT, const TermInfo* terms, int K, int n1,
+                                  int n2, int n3) {
+  for (int k = 0; k < K; ++k) {
+    const TermInfo& t = terms[k];
+    for2d(n1, t.r1, [&](int i, int c) {
+      int p = 0, q = c;
+      if (t.fb) {
+        p = c / t.b1;
+        q = c - p * t.b1;
+      }
+      const int ii = t.refl == 1 ? n1 - 1 - i : i;
+      double v = t.scale * t.base[ii + n1 * q];
+      if (t.u[0]) v *= t.u[0][i];
+      if (t.fb) v *= t.fb[i + n1 * p];
+      F[i + n1 * (t.off1 + c)] = v;
+    });
+    const double* L = t.base + (long long)n1 * t.b1 + (long long)n2 * t.b1 * t.b2;
+    const double* FL =
+        t.fb ? t.fb + (long long)n1 * t.fa1 + (long long)n2 * t.fa1 * t.fa2 : nullptr;
+    for2d(t.r2, n3, [&](int c, int kk) {  // coalesced read of last (c fastest)
+      int p = 0, q = c;
+      if (t.fb) {
+        p = c / t.b2;
+        q = c - p * t.b2;
+      }
+      const int kr = t.refl == 3 ? n3 - 1 - kk : kk;
+      double v = L[q + t.b2 * kr];
+      if (t.u[2]) v *= t.u[2][kk];
+      if (FL) v *= FL[p + t.fa2 * kk];
+      lastT[kk + n3 * (t.off2 + c)] = v;
+    });
+  }
 }
+
 
 // Householder QR of A (m x ncols, col-major, lda) in place: R in the upper
 // triangle, reflector tails below the diagonal, tau[k].
@@ -356,130 +357,6 @@ __device__ void qrp_inplace(double* M, int ldm, int p, int m, double* vn, int* p
   }
 }
 
-// One-sided (Hestenes) Jacobi on the columns of X (m x c, ld ldx) with
-// tracked squared column norms (one dot product per pair and round; the
-// norms are refreshed at every sweep).
-template <int TPP>
-__device__ int jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
-  const int cp = c + (c & 1);
-  const int npairs = cp / 2;
-  const int pi = threadIdx.x / TPP, sub = threadIdx.x % TPP;
-  const double tol2 = 1e-30;  // (1e-15)^2, |gamma| > 1e-15 sqrt(alpha beta)
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    for (int j = threadIdx.x; j < c; j += NT) {
-      double s = 0.0;
-      for (int i = 0; i < m; ++i) s += X[i + ldx * j] * X[i + ldx * j];
-      nrm[j] = s;
-    }
-    __syncthreads();
-    bool rotated = false;
-    bool big = false;  // some rotation in this sweep had |gamma| > 1e-9 sqrt(alpha beta)
-    for (int r = 0; r < cp - 1; ++r) {
-      for (int base = 0; base < npairs; base += NT / TPP) {
-        const int pp = base + pi;
-        // round-robin pairs: a = (pp + r - 1) mod (cp - 1) + 1 (pp > 0),
-        // b = (cp - 2 - pp + r) mod (cp - 1) + 1; both arguments < 2 (cp - 1)
-        int a = pp + r - 1;
-        if (a >= cp - 1) a -= cp - 1;
-        a = pp == 0 ? 0 : a + 1;
-        int b = cp - 2 - pp + r;
-        if (b >= cp - 1) b -= cp - 1;
-        b += 1;
-        const bool live = pp < npairs && a < c && b < c;
-        double ga = 0.0;
-        double* x = X + ldx * (live ? a : 0);
-        double* y = X + ldx * (live ? b : 0);
-        if (live)
-          for (int i = sub; i < m; i += TPP) ga += x[i] * y[i];
-        ga = group_sum<TPP>(ga);
-        if (live && ga != 0.0) {
-          const double al = nrm[a], be = nrm[b];
-          if (ga * ga > tol2 * al * be) {
-            big = big || (ga * ga > 1e-18 * al * be);
-            // t = sign(d) 2 ga / (|d| + sqrt(d^2 + 4 ga^2)), d = be - al: the
-            // angle needs no more than FP32 accuracy (an inexact angle only
-            // slows convergence); cs, sn are normalised in FP64 so the
-            // rotation stays orthogonal to working precision.
-            const double d = be - al;
-            const double mag = fmax(fabs(d), 2.0 * fabs(ga));
-            const int ex = (int)((__double_as_longlong(mag) >> 52) & 0x7ff) - 1023;
-            const double sc = __longlong_as_double((long long)(1023 - ex) << 52);
-            const float df = (float)(d * sc), gf = (float)(ga * sc);
-            const float tf = copysignf(1.0f, df) * (2.0f * gf) /
-                             (fabsf(df) + sqrtf(df * df + 4.0f * gf * gf));
-            const double t = (double)tf;
-            rotated = rotated || (tf != 0.0f);  // an FP32-underflowed angle is converged
-            const double cs = fast_rsqrt(1.0 + t * t), sn = cs * t;
-            for (int i = sub; i < m; i += TPP) {
-              const double xi = x[i], yi = y[i];
-              x[i] = cs * xi - sn * yi;
-              y[i] = sn * xi + cs * yi;
-            }
-            if (sub == 0) {
-              const double c2 = cs * cs, tg = 2.0 * t * ga, t2 = t * t;
-              nrm[a] = c2 * (al - tg + t2 * be);
-              nrm[b] = c2 * (be + tg + t2 * al);
-            }
-          }
-        }
-      }
-      __syncthreads();
-    }
-    // rotations in this sweep were all below 1e-9 of the column norms: by
-    // the quadratic convergence of cyclic Jacobi the remaining couplings
-    // are O(1e-18), below the 1e-15 threshold -- no verification sweep
-    const int any_rot = __syncthreads_or(rotated ? 1 : 0);
-    const int any_big = __syncthreads_or(big ? 1 : 0);
-    if (!any_rot || !any_big) return sweep + 1;
-  }
-  return 60;
-}
-
-__device__ int jacobi(double* X, int ldx, int m, int c, double* nrm) {
-  const int npairs = (c + 1) / 2;
-  const int tpp = min(32, floor_pow2(max(1, NT / max(npairs, 1))));
-  switch (tpp) {
-    case 32: return jacobi_t<32>(X, ldx, m, c, nrm);
-    case 16: return jacobi_t<16>(X, ldx, m, c, nrm);
-    case 8: return jacobi_t<8>(X, ldx, m, c, nrm);
-    case 4: return jacobi_t<4>(X, ldx, m, c, nrm);
-    case 2: return jacobi_t<2>(X, ldx, m, c, nrm);
-    default: return jacobi_t<1>(X, ldx, m, c, nrm);
-  }
-}
-
-// proj/src/tt_tensor.cpp:18-29, plus the decision margin.
-__device__ int truncation_rank(const double* sigma, int len, double budget2, int cap,
-                               double* margin) {
-  int r = len;
-  double tail = 0.0;
-  double mg = INFINITY;
-  while (r > 1) {
-    const double s2 = sigma[r - 1] * sigma[r - 1];
-    if (tail + s2 > budget2) {
-      mg = fmin(mg, (tail + s2 - budget2));
-      break;
-    }
-    tail += s2;
-    --r;
-  }
-  mg = fmin(mg, budget2 - tail);
-  if (cap > 0 && r > cap) r = cap;
-  if (margin) *margin = budget2 > 0.0 ? mg / budget2 : INFINITY;
-  return r;
-}
-
-struct SvdWork {
-  unsigned long long* prof;  // optional sweep counter
-  double* Xs;    // mx x mx
-  double* vn;    // mx
-  double* sig;   // mx
-  double* sraw;  // mx
-  int* piv;      // mx
-  int* perm;     // mx
-  double* sh;
-  int ldx;
-};
 
 // Singular values and the leading left singular vectors of C = M^T, where
 // M is p x m (ld ldm, destroyed): M Pi = Q R, X = R^T (m x k), Jacobi on
@@ -551,10 +428,20 @@ __device__ void stage_slice(double* Ms, const TermInfo* terms, int K, int n1, in
   for (int k = 0; k < K; ++k) {
     const TermInfo& t = terms[k];
     const int jj = t.refl == 2 ? n2 - 1 - j : j;
-    const double* src = t.base + (long long)n1 * t.r1 + (long long)jj * t.r1 * t.r2;
+    const double* src = t.base + (long long)n1 * t.b1 + (long long)jj * t.b1 * t.b2;
     const double f = t.u[1] ? t.u[1][j] : 1.0;
-    const int sz = t.r1 * t.r2;
-    for (int e = threadIdx.x; e < sz; e += NT) Ms[t.ms + e] = f * src[e];
+    if (!t.fb) {
+      const int sz = t.r1 * t.r2;
+      for (int e = threadIdx.x; e < sz; e += NT) Ms[t.ms + e] = f * src[e];
+    } else {
+      // Kronecker block A2_j (x) B2_j: (p*b1 + q, p'*b2 + q') = A(p,p') B(q,q')
+      const double* fs = t.fb + (long long)n1 * t.fa1 + (long long)j * t.fa1 * t.fa2;
+      for2d(t.r1, t.r2, [&](int r, int c) {
+        const int p = r / t.b1, q = r - p * t.b1;
+        const int pp = c / t.b2, qq = c - pp * t.b2;
+        Ms[t.ms + r + t.r1 * c] = f * fs[p + t.fa1 * pp] * src[q + t.b1 * qq];
+      });
+    }
   }
 }
 
@@ -637,180 +524,6 @@ __device__ void times_r3t(double* out, int ldo, bool trans, const double* X, int
   });
 }
 
-// ---- double-double arithmetic for the exact Gram route -------------------
-__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
-  s = a + b;
-  const double bb = s - a;
-  e = (a - (s - bb)) + (b - bb);
-}
-
-// (hi, lo) += a * b with the product and the sum error kept in lo
-__device__ __forceinline__ void dd_fma_acc(double& hi, double& lo, double a, double b) {
-  const double p = a * b;
-  const double pe = fma(a, b, -p);
-  double s, e;
-  two_sum(hi, p, s, e);
-  hi = s;
-  lo += e + pe;
-}
-
-__device__ __forceinline__ void dd_norm(double& hi, double& lo) {
-  double s, e;
-  two_sum(hi, lo, s, e);
-  hi = s;
-  lo = e;
-}
-
-// (a_hi, a_lo) * (b_hi, b_lo) -> (p, pe), unnormalised
-__device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl, double& p,
-                                       double& pe) {
-  p = ah * bh;
-  pe = fma(ah, bh, -p) + (ah * bl + al * bh);
-}
-
-// Visit the upper triangle (i <= j) of a d x d matrix: entry e -> (i, j).
-__device__ __forceinline__ void tri_index(int e, int d, int& i, int& j) {
-  int row = 0, len = d;
-  while (e >= len) {
-    e -= len;
-    ++row;
-    --len;
-  }
-  i = row;
-  j = row + e;
-}
-
-// Pivoted Cholesky of the symmetric PSD matrix G (d x d, hi/lo planes, ld
-// d) in double-double: Pi^T G Pi = R^T R, stopping when the largest
-// remaining pivot is <= thresh.  R (k x d, ld ldr, columns in pivoted
-// order) is rounded to double; piv[v] = original index of virtual column v.
-// Returns the rank k.
-__device__ int chol_piv_dd(double* Gh, double* Gl, int d, double thresh, double* R, int ldr,
-                           int* piv, double* sh) {
-  for (int t = threadIdx.x; t < d; t += NT) piv[t] = t;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  int k = 0;
-  for (; k < d; ++k) {
-    double bv = -1.0;
-    int bi = k;
-    for (int v = k + lane; v < d; v += 32) {
-      const int o = piv[v];
-      const double g = Gh[o + d * o];
-      if (g > bv) {
-        bv = g;
-        bi = v;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if (!(bv > thresh)) break;  // uniform: every warp found the same maximum
-    __syncthreads();            // everyone has read piv
-    if (threadIdx.x == 0) {
-      const int q = piv[k];
-      piv[k] = piv[bi];
-      piv[bi] = q;
-      for (int r = 0; r < k; ++r) {  // earlier rows of R follow the column swap
-        const double a = R[r + ldr * k];
-        R[r + ldr * k] = R[r + ldr * bi];
-        R[r + ldr * bi] = a;
-      }
-      const int o = piv[k];
-      const double ah = Gh[o + d * o], al = Gl[o + d * o];
-      const double s = sqrt(ah);
-      const double p = s * s, pe = fma(s, s, -p);
-      const double r = ((ah - p) - pe + al) * (0.5 / s);
-      double sh_, sl_;
-      two_sum(s, r, sh_, sl_);
-      sh[0] = sh_;
-      sh[1] = sl_;
-      sh[2] = 1.0 / sh_;
-    }
-    __syncthreads();
-    const int pk = piv[k];
-    const double rh = sh[0], rl = sh[1], rinv = sh[2];
-    // row k: R_kj = G[pk, p_j] / r_kk, kept in G's row pk (dd)
-    for (int v = k + 1 + threadIdx.x; v < d; v += NT) {
-      const int o = piv[v];
-      const double ah = Gh[pk + d * o], al = Gl[pk + d * o];
-      const double q1 = ah * rinv;
-      double p, pe;
-      dd_mul(q1, 0.0, rh, rl, p, pe);
-      const double res = ((ah - p) - pe) + al;
-      const double q2 = res * rinv;
-      double qh, ql;
-      two_sum(q1, q2, qh, ql);
-      Gh[pk + d * o] = qh;
-      Gl[pk + d * o] = ql;
-      R[k + ldr * v] = qh + ql;
-    }
-    if (threadIdx.x == 0) R[k + ldr * k] = rh + rl;
-    __syncthreads();
-    // trailing update G[p_i, p_j] -= R_ki R_kj, i, j > k
-    const int m = d - k - 1;
-    for2d(m, m, [&](int a, int b) {
-      const int oi = piv[k + 1 + a], oj = piv[k + 1 + b];
-      double p, pe;
-      dd_mul(Gh[pk + d * oi], Gl[pk + d * oi], Gh[pk + d * oj], Gl[pk + d * oj], p, pe);
-      double s, e;
-      two_sum(Gh[oi + d * oj], -p, s, e);
-      double lo = Gl[oi + d * oj] + e - pe;
-      dd_norm(s, lo);
-      Gh[oi + d * oj] = s;
-      Gl[oi + d * oj] = lo;
-    });
-    __syncthreads();
-  }
-  return k;
-}
-
-// Singular values and leading left singular vectors of C from the factor R
-// (k x m, ld ldr, pivoted columns piv) with C C^T = Pi R^T R Pi^T: Jacobi
-// on X = R^T, U_C = Pi * normalised columns of X (svd_left without the QR).
-__device__ int svd_from_r(const double* R, int ldr, int k, int m, const int* piv,
-                          const SvdWork& w, double budget2, int cap, double* U, int ldu,
-                          double* margin_out, int* s_int) {
-  for2d(m, k, [&](int i, int r) { w.Xs[i + w.ldx * r] = i >= r ? R[r + ldr * i] : 0.0; });
-  __syncthreads();
-  const int sweeps = jacobi(w.Xs, w.ldx, m, k, w.vn);
-  if (w.prof && threadIdx.x == 0) {
-    atomicAdd(&w.prof[12], (unsigned long long)sweeps);
-    atomicAdd(&w.prof[13], 1ULL);
-    if (sweeps >= 60) atomicAdd(&w.prof[14], 1ULL);
-  }
-  for (int q = threadIdx.x; q < k; q += NT) {
-    double s = 0.0;
-    for (int i = 0; i < m; ++i) s += w.Xs[i + w.ldx * q] * w.Xs[i + w.ldx * q];
-    w.sraw[q] = sqrt(s);
-  }
-  __syncthreads();
-  for (int q = threadIdx.x; q < k; q += NT) {
-    const double v = w.sraw[q];
-    int rank = 0;
-    for (int o = 0; o < k; ++o) {
-      const double u = w.sraw[o];
-      rank += (u > v) || (u == v && o < q);
-    }
-    w.sig[rank] = v;
-    w.perm[rank] = q;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) *s_int = truncation_rank(w.sig, k, budget2, cap, margin_out);
-  __syncthreads();
-  const int t = *s_int;
-  for2d(m, t, [&](int i, int r) {
-    U[piv[i] + ldu * r] = w.Xs[i + w.ldx * w.perm[r]] / w.sig[r];
-  });
-  __syncthreads();
-  return t;
-}
 
 // Gram accumulation of the rows of T (rows x ncol, ld ldt) into the
 // register-resident upper-triangle entries (ei, ej) of this thread.
@@ -887,61 +600,9 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
     atomicAdd(&p.prof[k], (unsigned long long)(t_ - prof_t));        \
     prof_t = t_;                                                     \
   }
-  const long long t0 = p.term_off ? p.term_off[o] : o;
-  const int K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
-
-  if (threadIdx.x == 0) {
-    int off1 = 0, off2 = 0, ms = 0;
-    for (int k = 0; k < K; ++k) {
-      const Term tm = p.terms[t0 + k];
-      const TSet& s = p.sets[tm.set];
-      TermInfo ti;
-      ti.r1 = s.ranks[2 * tm.idx];
-      ti.r2 = s.ranks[2 * tm.idx + 1];
-      ti.base = s.base + s.off[tm.idx];
-      double sc = tm.scale * s.uscale;
-      if (s.tscale) sc *= s.tscale[tm.idx];
-      ti.scale = sc;
-      ti.refl = tm.refl;
-      const double* fac = tm.fac >= 0 ? p.factors + (long long)tm.fac * (n1 + n2 + n3) : nullptr;
-      ti.u[0] = fac ? fac : nullptr;
-      ti.u[1] = fac ? fac + n1 : nullptr;
-      ti.u[2] = fac ? fac + n1 + n2 : nullptr;
-      ti.off1 = off1;
-      ti.off2 = off2;
-      ti.ms = ms;
-      off1 += ti.r1;
-      off2 += ti.r2;
-      ms += ti.r1 * ti.r2;
-      terms[k] = ti;
-    }
-    s_meta[0] = off1;
-    s_meta[1] = off2;
-  }
-  __syncthreads();
-  const int R1 = s_meta[0], R2 = s_meta[1];
-  for (int k = 0; k < K; ++k) {
-    const TermInfo& t = terms[k];
-    for (int a = threadIdx.x; a < t.r1; a += NT) rowterm[t.off1 + a] = k;
-    for (int b = threadIdx.x; b < t.r2; b += NT) colterm[t.off2 + b] = k;
-  }
-  // ---- materialise F (n1 x R1) and last^T (n3 x R2) ----
-  for (int k = 0; k < K; ++k) {
-    const TermInfo& t = terms[k];
-    for2d(n1, t.r1, [&](int i, int a) {
-      const int ii = t.refl == 1 ? n1 - 1 - i : i;
-      double v = t.scale * t.base[ii + n1 * a];
-      if (t.u[0]) v *= t.u[0][i];
-      F[i + n1 * (t.off1 + a)] = v;
-    });
-    const double* L = t.base + (long long)n1 * t.r1 + (long long)n2 * t.r1 * t.r2;
-    for2d(t.r2, n3, [&](int b, int kk) {  // coalesced read of last (b fastest)
-      const int kr = t.refl == 3 ? n3 - 1 - kk : kk;
-      double v = L[b + t.r2 * kr];
-      if (t.u[2]) v *= t.u[2][kk];
-      lastT[kk + n3 * (t.off2 + b)] = v;
-    });
-  }
+  int K, R1, R2;
+  setup_terms(p, o, terms, rowterm, colterm, s_meta, K, R1, R2);
+  materialise_outer(F, lastT, terms, K, n1, n2, n3);
   __syncthreads();
   PROF(0);
   // ---- 1. QR of last^T ----
@@ -1088,8 +749,11 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
     if (p.acc) {
       double in_sz = 0.0;
       for (int k = 0; k < K; ++k)
-        in_sz += (double)n1 * terms[k].r1 + (double)n2 * terms[k].r1 * terms[k].r2 +
-                 (double)terms[k].r2 * n3;
+        in_sz += (double)n1 * terms[k].b1 + (double)n2 * terms[k].b1 * terms[k].b2 +
+                 (double)terms[k].b2 * n3 +
+                 (terms[k].fb ? (double)n1 * terms[k].fa1 + (double)n2 * terms[k].fa1 * terms[k].fa2 +
+                                    (double)terms[k].fa2 * n3
+                              : 0.0);
       atomicAdd(&p.acc[0], round_flops((double)n2, (double)R1, (double)R2, (double)t1, (double)t2));
       atomicAdd(&p.acc[1], 8.0 * (in_sz + (double)sz));
     }
@@ -1207,60 +871,9 @@ __global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
     atomicAdd(&p.prof[k], (unsigned long long)(t_ - prof_t));        \
     prof_t = t_;                                                     \
   }
-  const long long t0 = p.term_off ? p.term_off[o] : o;
-  const int K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
-
-  if (threadIdx.x == 0) {
-    int off1 = 0, off2 = 0, ms = 0;
-    for (int k = 0; k < K; ++k) {
-      const Term tm = p.terms[t0 + k];
-      const TSet& s = p.sets[tm.set];
-      TermInfo ti;
-      ti.r1 = s.ranks[2 * tm.idx];
-      ti.r2 = s.ranks[2 * tm.idx + 1];
-      ti.base = s.base + s.off[tm.idx];
-      double sc = tm.scale * s.uscale;
-      if (s.tscale) sc *= s.tscale[tm.idx];
-      ti.scale = sc;
-      ti.refl = tm.refl;
-      const double* fac = tm.fac >= 0 ? p.factors + (long long)tm.fac * (n1 + n2 + n3) : nullptr;
-      ti.u[0] = fac ? fac : nullptr;
-      ti.u[1] = fac ? fac + n1 : nullptr;
-      ti.u[2] = fac ? fac + n1 + n2 : nullptr;
-      ti.off1 = off1;
-      ti.off2 = off2;
-      ti.ms = ms;
-      off1 += ti.r1;
-      off2 += ti.r2;
-      ms += ti.r1 * ti.r2;
-      terms[k] = ti;
-    }
-    s_meta[0] = off1;
-    s_meta[1] = off2;
-  }
-  __syncthreads();
-  const int R1 = s_meta[0], R2 = s_meta[1];
-  for (int k = 0; k < K; ++k) {
-    const TermInfo& t = terms[k];
-    for (int a = threadIdx.x; a < t.r1; a += NT) rowterm[t.off1 + a] = k;
-    for (int b = threadIdx.x; b < t.r2; b += NT) colterm[t.off2 + b] = k;
-  }
-  for (int k = 0; k < K; ++k) {
-    const TermInfo& t = terms[k];
-    for2d(n1, t.r1, [&](int i, int a) {
-      const int ii = t.refl == 1 ? n1 - 1 - i : i;
-      double v = t.scale * t.base[ii + n1 * a];
-      if (t.u[0]) v *= t.u[0][i];
-      F[i + n1 * (t.off1 + a)] = v;
-    });
-    const double* L = t.base + (long long)n1 * t.r1 + (long long)n2 * t.r1 * t.r2;
-    for2d(t.r2, n3, [&](int b, int kk) {
-      const int kr = t.refl == 3 ? n3 - 1 - kk : kk;
-      double v = L[b + t.r2 * kr];
-      if (t.u[2]) v *= t.u[2][kk];
-      lastT[kk + n3 * (t.off2 + b)] = v;
-    });
-  }
+  int K, R1, R2;
+  setup_terms(p, o, terms, rowterm, colterm, s_meta, K, R1, R2);
+  materialise_outer(F, lastT, terms, K, n1, n2, n3);
   __syncthreads();
   PROF(0);
   qr_inplace(lastT, n3, n3, R2, tau, sh);
@@ -1385,8 +998,11 @@ __global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
     if (p.acc) {
       double in_sz = 0.0;
       for (int k = 0; k < K; ++k)
-        in_sz += (double)n1 * terms[k].r1 + (double)n2 * terms[k].r1 * terms[k].r2 +
-                 (double)terms[k].r2 * n3;
+        in_sz += (double)n1 * terms[k].b1 + (double)n2 * terms[k].b1 * terms[k].b2 +
+                 (double)terms[k].b2 * n3 +
+                 (terms[k].fb ? (double)n1 * terms[k].fa1 + (double)n2 * terms[k].fa1 * terms[k].fa2 +
+                                    (double)terms[k].fa2 * n3
+                              : 0.0);
       atomicAdd(&p.acc[0], round_flops((double)n2, (double)R1, (double)R2, (double)t1, (double)t2));
       atomicAdd(&p.acc[1], 8.0 * (in_sz + (double)sz));
     }
@@ -1503,7 +1119,11 @@ __global__ void round_bounds_kernel(RoundArgs p, int* bounds) {
     for (int k = 0; k < K; ++k) {
       const Term tm = p.terms[t0 + k];
       const TSet& s = p.sets[tm.set];
-      const int a = s.ranks[2 * tm.idx], b = s.ranks[2 * tm.idx + 1];
+      int a = s.ranks[2 * tm.idx], b = s.ranks[2 * tm.idx + 1];
+      if (tm.fset >= 0) {
+        a *= p.sets[tm.fset].ranks[2 * tm.fidx];
+        b *= p.sets[tm.fset].ranks[2 * tm.fidx + 1];
+      }
       r1 += a;
       r2 += b;
       ms += a * b;

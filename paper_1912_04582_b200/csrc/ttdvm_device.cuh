@@ -6,7 +6,7 @@
 
 namespace ttdvm {
 
-constexpr int kMaxSets = 8;
+constexpr int kMaxSets = 12;
 constexpr int kMaxTerms = 16;     // summands per rounded output
 constexpr int kRoundThreads = 128;
 
@@ -19,16 +19,23 @@ struct TSet {
   double uscale;           // uniform scale (e.g. dt for R)
 };
 
-// One summand of a rounded output: scale * (factor o reflect(set[idx])).
-// factor (>= 0) indexes a rank-1 face factor u1 (x) u2 (x) u3 in
+// One summand of a rounded output:
+//   scale * dscale[dsi] * (fset[fidx] o factor o reflect(set[idx])).
+// factor (fac >= 0) indexes a rank-1 face factor u1 (x) u2 (x) u3 in
 // RoundArgs::factors (the axis-aligned (xi.n)^{+/-});
-// refl (1..3) is the specular-ghost index reversal (T9 / T20).
+// fset >= 0 names a TT Hadamard factor (oblique-normal xi_n and |xi_n|
+// estimate, T12/T13) taken from another set; refl (1..3) is the specular-
+// ghost index reversal (T9 / T20) of the set[idx] operand; dsi >= 0 picks a
+// per-step scale computed on the device (the wall-ghost density n_w, T19).
 struct Term {
   int set;
   int idx;
   double scale;
-  int fac;
-  int refl;
+  int fac = -1;
+  int refl = 0;
+  int fset = -1;
+  int fidx = 0;
+  int dsi = -1;
 };
 
 struct RoundOut {
@@ -46,15 +53,25 @@ enum StatusWord {
   kStMaxR2 = 2,
   kStError = 3,     // 0 ok, else error code (see kErr*)
   kStErrIdx = 4,    // index of the first failing item
+  kStAux = 5,       // kernel-specific counter (face factors: imprecise normals)
   kStWords = 8
 };
-enum ErrCode { kErrNone = 0, kErrDensity = 1, kErrTemperature = 2, kErrNonFinite = 3 };
+enum ErrCode {
+  kErrNone = 0,
+  kErrDensity = 1,
+  kErrTemperature = 2,
+  kErrNonFinite = 3,
+  kErrZeroFactor = 4,      // face factor of an all-zero operand
+  kErrWallDegenerate = 5,  // wall_ghost: degenerate wall Maxwellian flux
+  kErrWallDensity = 6      // wall_ghost: nonpositive balance density
+};
 
 struct RoundArgs {
   TSet sets[kMaxSets];
   const long long* term_off;    // [nout+1] CSR into terms
   const Term* terms;
   const double* factors;        // [nfac][n1+n2+n3]
+  const double* dscale;         // per-step device scales (Term::dsi)
   int n1, n2, n3;
   int nout;
   double eps;

@@ -33,6 +33,7 @@ EXPORTS = (
     "ttdvm_cuda_launch_count", "ttdvm_cuda_set_profiling", "ttdvm_cuda_phase_work",
     "ttdvm_cuda_timed_step", "ttdvm_cuda_fp64_peak", "ttdvm_cuda_round_profile",
     "ttdvm_cuda_set_owned", "ttdvm_cuda_halo_pack", "ttdvm_cuda_halo_unpack",
+    "ttdvm_cuda_face_factors", "ttdvm_cuda_wall_densities", "ttdvm_cuda_setup_info",
 )
 
 OK, EINVAL, EDOMAIN, ENOMEM, ECUDA, ENCCL = range(6)
@@ -93,6 +94,9 @@ def load_library(path: str = LIB_PATH):
         "ttdvm_cuda_set_owned": (C.c_int, [vp, i32]),
         "ttdvm_cuda_halo_pack": (C.c_int, [vp, i32, vp, vp, vp, vp, i64]),
         "ttdvm_cuda_halo_unpack": (C.c_int, [vp, i32, vp, vp, vp, vp]),
+        "ttdvm_cuda_face_factors": (C.c_int, [vp, i32, vp, i32, i32, vp]),
+        "ttdvm_cuda_wall_densities": (C.c_int, [vp, vp]),
+        "ttdvm_cuda_setup_info": (C.c_int, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -287,6 +291,35 @@ class Context:
         jr = self._fetch(b.count, lambda r, o: self.lib.ttdvm_cuda_result_layout(self.h, r, o),
                          lambda c, cap: self.lib.ttdvm_cuda_result_download(self.h, c, cap))
         return jr, mac[:b.count]
+
+    def face_factors(self, normals, cap: int = 4, mode: str = "abs", diag: bool = False):
+        """VelocityGrid::abs_xi_estimate(normal, cap) ("abs"),
+        xi_normal_positive / xi_normal_negative(normal, cap - 2) ("pos" /
+        "neg", i.e. from_full(max/min(xi_n, 0), 1e-12, cap)) for a batch
+        of unit normals (proj/src/velocity_grid.cpp:61-146)."""
+        nrm = np.ascontiguousarray(np.asarray(normals, dtype=np.float64).reshape(-1, 3))
+        cnt = nrm.shape[0]
+        m = {"abs": 0, "pos": 1, "neg": 2}[mode]
+        dg = np.zeros(4 * max(cnt, 1)) if diag else None
+        self._check(self.lib.ttdvm_cuda_face_factors(self.h, cnt, _ptr(nrm), int(cap), m, _ptr(dg)))
+        out = self._fetch(cnt, lambda r, o: self.lib.ttdvm_cuda_result_layout(self.h, r, o),
+                          lambda c, cap_: self.lib.ttdvm_cuda_result_download(self.h, c, cap_))
+        if diag:
+            return out, dg[:4 * cnt].reshape(cnt, 4)
+        return out
+
+    def setup_info(self) -> dict:
+        info = np.zeros(4, dtype=np.int64)
+        self._check(self.lib.ttdvm_cuda_setup_info(self.h, _ptr(info)))
+        return dict(oblique_normals=int(info[0]), imprecise_normals=int(info[1]),
+                    wall_faces=int(info[2]), face_factor_ms=float(info[3]) / 1000.0)
+
+    def wall_densities(self) -> np.ndarray:
+        """n_w of the last step per wall face, in face order."""
+        nw = self.setup_info()["wall_faces"]
+        out = np.zeros(max(nw, 1))
+        self._check(self.lib.ttdvm_cuda_wall_densities(self.h, _ptr(out)))
+        return out[:nw]
 
     def phase_times(self) -> np.ndarray:
         out = np.zeros(8)

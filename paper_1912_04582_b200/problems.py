@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .mesh import Mesh, structured_box
+from .mesh import Mesh, obstacle_mesh, structured_box
 from .tt_batch import TtBatch
 
 GAS_M = 1.0
@@ -140,6 +140,30 @@ def periodic_box(shape=(32, 32, 32), nv: int = 24, bound: float = 6.0, kn: float
                    cfl_dt(mesh, bound), eps, cap, steps)
 
 
+def obstacle_flow(shape=(100, 80, 64), hole: int = 8, nv: int = 44, bound: float = 7.0,
+                  kn: float = 0.05, eps: float = 1e-5, mach: float = 3.0, steps: int = 20,
+                  seed: int = 4, jitter: float = 0.1, t_wall: float = 1.0,
+                  name="config4-obstacle-mach3") -> Problem:
+    """Config 4: jittered, shuffled hex mesh around a hole^3 rigid box
+    (mesh.obstacle_mesh), free-stream Maxwellian at Mach ``mach`` along +x
+    (u = mach * sqrt(5/3 R T), T = 1, n = 1) on the outer faces, diffuse
+    walls at T_w on the obstacle, impulsive start (the free stream in every
+    cell).  Kn is referred to the obstacle edge (L_ref = hole * h)."""
+    mesh = obstacle_mesh(shape, hole=hole, jitter=jitter, seed=seed)
+    dxi = 2.0 * bound / (nv - 1)
+    nodes = np.array([-bound + i * dxi for i in range(nv)])
+    u0 = mach * math.sqrt(5.0 / 3.0 * GAS_R * 1.0)
+    u = np.zeros((mesh.ncell, 3))
+    u[:, 0] = u0
+    f1, f2, f3 = maxwell_factors(nodes, np.ones(mesh.ncell), np.ones(mesh.ncell), u)
+    f0 = TtBatch.from_rank_one(f1, f2, f3)
+    free = dict(n=1.0, t=1.0, u=(u0, 0.0, 0.0))
+    bcs = [dict(kind="in", **free), dict(kind="out", **free), dict(kind="wall", t_wall=t_wall)]
+    return Problem(name, mesh, nv, bound, gas_params(kn, float(hole)), bcs, f0,
+                   cfl_dt(mesh, bound), eps, 0, steps, meta=dict(mach=mach, jitter=jitter,
+                                                                 hole=hole, seed=seed))
+
+
 def config(idx: int, scale: float = 1.0) -> Problem:
     """BASELINE.json configs by 1-based index; ``scale`` < 1 shrinks the
     spatial mesh for parity tests (velocity mesh unchanged)."""
@@ -148,6 +172,12 @@ def config(idx: int, scale: float = 1.0) -> Problem:
     if idx == 2:
         s = max(2, int(round(32 * scale)))
         return periodic_box((s, s, s))
+    if idx == 4:
+        if scale >= 1.0:
+            return obstacle_flow()
+        sx, sy, sz = (max(4, int(round(v * scale))) for v in (100, 80, 64))
+        hole = max(2, int(round(8 * scale)))
+        return obstacle_flow((sx, sy, sz), hole=hole)
     if idx == 5:
         sx, sy, sz = (max(2, int(round(v * scale))) for v in (128, 128, 64))
         return periodic_box((sx, sy, sz), nv=64, bound=8.0, kn=0.1, eps=1e-5, steps=10,
