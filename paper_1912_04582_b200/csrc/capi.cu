@@ -26,8 +26,9 @@
 
 namespace ttdvm {
 cudaError_t launch_round(const RoundArgs& a, cudaStream_t st);
-cudaError_t launch_round_bounds(const RoundArgs& a, int* bounds, cudaStream_t st);
-cudaError_t launch_round_gram(const RoundArgs& a, cudaStream_t st);
+cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st);
+cudaError_t launch_round_bins(const RoundArgs& a, int* counts, int* bmax, int* lists,
+                              cudaStream_t st);
 size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX);
 size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int MSMAX);
 struct MacroArgs {
@@ -246,6 +247,7 @@ struct ttdvm_ctx {
   DevBuf<int> d_status;
   int* h_status = nullptr;  // pinned, kStWords + 2 longs
   DevBuf<double> d_margins;
+  DevBuf<int> d_bins, d_olist;  // rank bins of the current rounding launch
   DevBuf<long long> d_tmp_off;
   DevBuf<double> d_tmp;
   bool profiling = false;
@@ -375,50 +377,60 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   a.margins = margins_dev;
   a.acc = c->d_acc.p;
   a.prof = c->round_prof ? c->d_prof.p : nullptr;
-  // exact per-launch bounds of the summed ranks (one tiny kernel + readback)
-  CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
-  CK(launch_round_bounds(a, c->d_status.p, c->st));
+  // rank bins: per-bin shared-memory plans (one tiny kernel + readback)
+  c->d_bins.alloc((size_t)kRankBins * 5);
+  c->d_olist.alloc((size_t)kRankBins * nout);
+  CK(cudaMemsetAsync(c->d_bins.p, 0, kRankBins * 5 * sizeof(int), c->st));
+  CK(launch_round_bins(a, c->d_bins.p, c->d_bins.p + kRankBins, c->d_olist.p, c->st));
   c->launches += 1;
-  CK(cudaMemcpyAsync(c->h_status, c->d_status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  int hb[kRankBins * 5];
+  CK(cudaMemcpyAsync(hb, c->d_bins.p, sizeof(hb), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  const int RM1 = std::max(1, c->h_status[0]);
-  const int RM2 = std::max(1, c->h_status[1]);
-  const int MSMAX = std::max(1, c->h_status[2]);
+  const int* bcount = hb;
+  const int* bmax = hb + kRankBins;
+  int RM1 = 1, RM2 = 1, MSMAX = 1;
+  for (int b = 0; b < kRankBins; ++b) {
+    if (!bcount[b]) continue;
+    RM1 = std::max(RM1, bmax[4 * b]);
+    RM2 = std::max(RM2, bmax[4 * b + 1]);
+    MSMAX = std::max(MSMAX, bmax[4 * b + 2]);
+  }
   const int mx = n;
-  // TSQR block height: as tall as the shared-memory budget allows, aiming
-  // at >= 3 resident CTAs per SM
+  if (mx > 48) throw Fail{TTDVM_EINVAL, "velocity grids above 48 nodes per axis are not supported"};
   // exact-Gram route by default; TTDVM_ROUND=tsqr selects the Householder
-  // TSQR route (kept for A/B comparison)
+  // TSQR route (kept for A/B comparison; one launch, global bounds)
   static const bool use_tsqr = [] {
     const char* e = getenv("TTDVM_ROUND");
     return e && std::string(e) == "tsqr";
   }();
   int HMAX = mx;
-  size_t smem;
   if (use_tsqr) {
-    if (mx > 48)
-      throw Fail{TTDVM_EINVAL, "velocity grids above 48 nodes per axis are not supported"};
     HMAX = mx <= 32 ? mx : 48;
-    smem = round_smem_bytes(n, n, n, RM1, RM2, HMAX, MSMAX);
-  } else {
-    if (mx > 48)
-      throw Fail{TTDVM_EINVAL, "velocity grids above 48 nodes per axis are not supported"};
-    smem = round_gram_smem_bytes(n, n, RM1, RM2, MSMAX);
+    if (round_smem_bytes(n, n, n, RM1, RM2, HMAX, MSMAX) > 227 * 1024)
+      throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory"};
   }
-  if (smem > 227 * 1024)
-    throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory (n=" + std::to_string(n) +
-                                 ", summed ranks " + std::to_string(RM1) + "x" +
-                                 std::to_string(RM2) + ")"};
-  a.RM1 = RM1;
-  a.RM2 = RM2;
+  struct Launch {
+    int bin, count, rm1, rm2, ms;
+  };
+  std::vector<Launch> plan;
+  for (int b = kRankBins - 1; b >= 0; --b) {  // large ranks first (long CTAs start early)
+    if (!bcount[b]) continue;
+    const Launch l{b, bcount[b], std::max(1, bmax[4 * b]), std::max(1, bmax[4 * b + 1]),
+                   std::max(1, bmax[4 * b + 2])};
+    if (!use_tsqr && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms) > 227 * 1024)
+      throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory (n=" +
+                                   std::to_string(n) + ", summed ranks " +
+                                   std::to_string(l.rm1) + "x" + std::to_string(l.rm2) + ")"};
+    plan.push_back(l);
+  }
   a.HMAX = HMAX;
-  a.MSMAX = MSMAX;
-  // arena estimate
+  // arena: a modest first estimate; an overflowing launch reports the exact
+  // total (the bump counter keeps counting), so one retry always suffices
   if (out.arena.n == 0) {
-    const int re = std::min(n, std::max(8, std::max(RM1, RM2) / std::max(1, tl.maxk) + 4));
+    const int re = std::min(n, 4);
     out.arena.alloc((size_t)nout * tt_size(n, n, n, re, re) + 1024);
   }
-  for (int attempt = 0; attempt < 8; ++attempt) {
+  for (int attempt = 0; attempt < 4; ++attempt) {
     a.out.ranks = out.ranks.p;
     a.out.off = out.off.p;
     a.out.base = out.arena.p;
@@ -426,8 +438,23 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     a.out.capacity = (long long)out.arena.n;
     CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
     CK(cudaMemsetAsync(c->d_acc.p, 0, 2 * sizeof(double), c->st));
-    CK(use_tsqr ? launch_round(a, c->st) : launch_round_gram(a, c->st));
-    c->launches += 1;
+    if (use_tsqr) {
+      a.RM1 = RM1;
+      a.RM2 = RM2;
+      a.MSMAX = MSMAX;
+      a.olist = nullptr;
+      CK(launch_round(a, c->st));
+      c->launches += 1;
+    } else {
+      for (const Launch& l : plan) {
+        a.RM1 = l.rm1;
+        a.RM2 = l.rm2;
+        a.MSMAX = l.ms;
+        a.olist = c->d_olist.p + (size_t)l.bin * nout;
+        CK(launch_round_gram(a, l.count, c->st));
+        c->launches += 1;
+      }
+    }
     CK(cudaMemcpyAsync(c->h_status, c->d_status.p, (kStWords + 4) * sizeof(int),
                        cudaMemcpyDeviceToHost, c->st));
     double acc[2];
@@ -436,12 +463,12 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     if (!c->h_status[kStOverflow]) {
       c->phase_flops[c->cur_phase] += acc[0];
       c->phase_bytes[c->cur_phase] += acc[1];
-      c->phase_launches[c->cur_phase] += 1;
+      c->phase_launches[c->cur_phase] += use_tsqr ? 1 : (int)plan.size();
     }
     const unsigned long long used =
         *reinterpret_cast<unsigned long long*>(c->h_status + kStWords);
     if (c->h_status[kStOverflow]) {
-      const size_t want = std::max<size_t>(out.arena.n * 2, (size_t)(used * 1.25) + 1024);
+      const size_t want = std::max<size_t>(out.arena.n + 1024, (size_t)(used * 1.1) + 1024);
       out.arena.free();
       out.arena.alloc(want);
       continue;
@@ -1111,6 +1138,8 @@ int ttdvm_cuda_destroy(ttdvm_ctx* c) {
   c->d_acc.free();
   c->d_prof.free();
   c->d_margins.free();
+  c->d_bins.free();
+  c->d_olist.free();
   c->d_tmp.free();
   c->d_tmp_off.free();
   if (c->h_status) cudaFreeHost(c->h_status);

@@ -187,7 +187,7 @@ __device__ int jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
   return 60;
 }
 
-__device__ int jacobi(double* X, int ldx, int m, int c, double* nrm) {
+__device__ __noinline__ int jacobi(double* X, int ldx, int m, int c, double* nrm) {
   const int npairs = (c + 1) / 2;
   const int tpp = min(32, floor_pow2(max(1, NT / max(npairs, 1))));
   switch (tpp) {
@@ -280,7 +280,7 @@ __device__ __forceinline__ void tri_index(int e, int d, int& i, int& j) {
 // remaining pivot is <= thresh.  R (k x d, ld ldr, columns in pivoted
 // order) is rounded to double; piv[v] = original index of virtual column v.
 // Returns the rank k.
-__device__ int chol_piv_dd(double* Gh, double* Gl, int d, double thresh, double* R, int ldr,
+__device__ __noinline__ int chol_piv_dd(double* Gh, double* Gl, int d, double thresh, double* R, int ldr,
                            int* piv, double* sh) {
   for (int t = threadIdx.x; t < d; t += NT) piv[t] = t;
   __syncthreads();
@@ -369,7 +369,7 @@ __device__ int chol_piv_dd(double* Gh, double* Gl, int d, double thresh, double*
 // Singular values and leading left singular vectors of C from the factor R
 // (k x m, ld ldr, pivoted columns piv) with C C^T = Pi R^T R Pi^T: Jacobi
 // on X = R^T, U_C = Pi * normalised columns of X (svd_left without the QR).
-__device__ int svd_from_r(const double* R, int ldr, int k, int m, const int* piv,
+__device__ __noinline__ int svd_from_r(const double* R, int ldr, int k, int m, const int* piv,
                           const SvdWork& w, double budget2, int cap, double* U, int ldu,
                           double* margin_out, int* s_int) {
   for2d(m, k, [&](int i, int r) { w.Xs[i + w.ldx * r] = i >= r ? R[r + ldr * i] : 0.0; });

@@ -143,7 +143,7 @@ __device__ void materialise_outer(double* F, double* lastT, const TermInfo* term
 
 // Householder QR of A (m x ncols, col-major, lda) in place: R in the upper
 // triangle, reflector tails below the diagonal, tau[k].
-__device__ void qr_inplace(double* A, int lda, int m, int ncols, double* tau, double* sh) {
+__device__ __noinline__ void qr_inplace(double* A, int lda, int m, int ncols, double* tau, double* sh) {
   const int kmax = min(m, ncols);
   for (int k = 0; k < kmax; ++k) {
     if (threadIdx.x < 32) {
@@ -270,7 +270,7 @@ __device__ void qr_update(double* R, int ldr, const double* B, int ldb, int h, i
 // Column-pivoted Householder QR of M (p x m, ld ldm) in place (dgeqp3
 // semantics, Q discarded): on exit the upper trapezoid holds R (k x m,
 // k = min(p, m)) of M Pi, piv[i] = original column at position i.
-__device__ void qrp_inplace(double* M, int ldm, int p, int m, double* vn, int* piv, double* sh) {
+__device__ __noinline__ void qrp_inplace(double* M, int ldm, int p, int m, double* vn, int* piv, double* sh) {
   const int kmax = min(p, m);
   for (int j = threadIdx.x; j < m; j += NT) {
     double s = 0.0;
@@ -362,7 +362,7 @@ __device__ void qrp_inplace(double* M, int ldm, int p, int m, double* vn, int* p
 // M is p x m (ld ldm, destroyed): M Pi = Q R, X = R^T (m x k), Jacobi on
 // X; C = Pi X Q^T so U_C = Pi * normalised columns of X.  Writes U (m x t,
 // ld ldu); returns the truncation rank (all threads).
-__device__ int svd_left(double* M, int ldm, int p, int m, const SvdWork& w, double budget2,
+__device__ __noinline__ int svd_left(double* M, int ldm, int p, int m, const SvdWork& w, double budget2,
                         int cap, double* U, int ldu, double* margin_out, int* s_int) {
   const int k = min(p, m);
   qrp_inplace(M, ldm, p, m, w.vn, w.piv, w.sh);
@@ -832,24 +832,28 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
 // accuracy of the QR route -- while the slice loop has no sequential
 // column steps (3 barriers per slice instead of 2 per column).
 template <int Q>
-__global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
+__global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_kernel(RoundArgs p) {
   extern __shared__ double sm[];
   const int n1 = p.n1, n2 = p.n2, n3 = p.n3;
   const int mx = max(n1, n3);
   const int RM1 = p.RM1, RM2 = p.RM2;
   const int RMX = max(RM1, RM2);
-  const int ZR = max(2 * mx, RM2);
+  // Buffers scale with D = max(min(n1, RM1), min(n3, RM2)) -- the largest
+  // Gram / SVD dimension of this launch -- not with n^2, so launches of
+  // low-rank sums (the rank bins of run_round) fit several CTAs per SM.
+  const int D1 = min(n1, RM1), D3 = min(n3, RM2), D = max(D1, D3);
+  const int GZ = max(2 * D * D, RM2 * D);
   double* F = sm;                          // n1 x RMX   (cut 2 / output: X2)
   double* lastT = F + n1 * RMX;            // n3 x RM2
   double* tau = lastT + n3 * RM2;          // mx
-  double* Tb = tau + mx;                   // mx x mx    (slice block; V2 at the end)
-  double* G = Tb + mx * mx;                // ZR x mx    (Gram hi/lo planes; Z at the end)
-  double* Gl = G + mx * mx;
-  double* XP = G + ZR * mx;                // n1 x RMX   (cut 1: X; cut 2: P)
-  double* U1 = XP + n1 * RMX;              // n1 x n1
-  double* Xs = U1 + n1 * n1;               // mx x mx
-  double* Rc = Xs + mx * mx;               // mx x mx    (Cholesky factor)
-  double* Ms = Rc + mx * mx;               // p.MSMAX
+  double* Tb = tau + mx;                   // mx x D     (slice blocks, C^T; V2 at the end)
+  double* G = Tb + mx * D;                 // GZ         (Gram hi/lo planes; Z at the end)
+  double* Gl = G + D * D;
+  double* XP = G + GZ;                     // n1 x RMX   (cut 1: X; cut 2: P)
+  double* U1 = XP + n1 * RMX;              // n1 x D1
+  double* Xs = U1 + n1 * D1;               // mx x D     (Jacobi workspace)
+  double* Rc = Xs + mx * D;                // D x D      (Cholesky factor)
+  double* Ms = Rc + D * D;                 // p.MSMAX
   double* sig = Ms + p.MSMAX;              // mx
   double* sraw = sig + mx;                 // mx
   double* vn = sraw + mx;                  // mx
@@ -862,7 +866,7 @@ __global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
       reinterpret_cast<double*>(rowterm + RM1 + (((RM1 + RM2) & 1) ? 1 : 0)));
   __shared__ int s_meta[8];
 
-  const int o = blockIdx.x;
+  const int o = p.olist ? p.olist[blockIdx.x] : blockIdx.x;
   if (o >= p.nout) return;
   long long prof_t = p.prof ? clock64() : 0;
 #define PROF(k)                                                      \
@@ -880,16 +884,24 @@ __global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
   const int q3 = min(n3, R2);
   PROF(1);
 
-  // ---- cut 1: G1 = sum_j T_j T_j^T (n1 x n1), T_j = F M_j R3^T ----
+  // ---- cut 1 ----
+  // T route (R1 >= n1): G1 = sum_j T_j T_j^T (n1 x n1), T_j = F M_j R3^T;
+  //   sigma(A_(1)) and U1 from its pivoted Cholesky factor.
+  // W route (R1 < n1): G_W = sum_j Z_j Z_j^T (R1 x R1), Z_j = M_j R3^T, so
+  //   A_(1) A_(1)^T = C C^T with C = F Pi R_W^T (n1 x k); sigma and U1 from
+  //   the column-pivoted QR + Jacobi of C^T (svd_left).  R1 x R1 work per
+  //   slice instead of n1 x n1 -- the common case of low-rank sums.
+  const bool wroute = R1 < n1;
+  const int d1 = wroute ? R1 : n1;
   int ei[Q], ej[Q];
   double gh[Q], gl[Q];
   {
-    const int ne = n1 * (n1 + 1) / 2;
+    const int ne = d1 * (d1 + 1) / 2;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int e = threadIdx.x + NT * q;
       gh[q] = gl[q] = 0.0;
-      if (e < ne) tri_index(e, n1, ei[q], ej[q]);
+      if (e < ne) tri_index(e, d1, ei[q], ej[q]);
       else ei[q] = ej[q] = -1;
     }
   }
@@ -897,19 +909,45 @@ __global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
     __syncthreads();
     stage_slice(Ms, terms, K, n1, n2, j);
     __syncthreads();
-    left_times_blockdiag(XP, n1, F, n1, n1, R2, Ms, terms, colterm);
+    if (wroute) {
+      // Z_j^T: Tb(a, c) = sum_b M_t(a, b) R3(c, off2 + b), R3 upper trapezoidal
+      for2d(R1, q3, [&](int a, int c) {
+        const TermInfo& t = terms[rowterm[a]];
+        const int aa = a - t.off1;
+        double s = 0.0;
+        for (int b = max(0, c - t.off2); b < t.r2; ++b)
+          s += lastT[c + n3 * (t.off2 + b)] * Ms[t.ms + aa + t.r1 * b];
+        Tb[a + d1 * c] = s;
+      });
+    } else {
+      left_times_blockdiag(XP, n1, F, n1, n1, R2, Ms, terms, colterm);
+      __syncthreads();
+      times_r3t(Tb, n1, false, XP, n1, n1, q3, R2, lastT, n3);
+    }
     __syncthreads();
-    times_r3t(Tb, n1, false, XP, n1, n1, q3, R2, lastT, n3);
-    __syncthreads();
-    gram_rows_acc<Q>(gh, gl, ei, ej, Tb, n1, q3);
+    gram_rows_acc<Q>(gh, gl, ei, ej, Tb, d1, q3);
   }
   __syncthreads();
-  gram_store<Q>(G, Gl, n1, gh, gl, ei, ej);
+  gram_store<Q>(G, Gl, d1, gh, gl, ei, ej);
   __syncthreads();
   PROF(2);
   double loc = 0.0;
-  for (int i = threadIdx.x; i < n1; i += NT) loc += G[i + n1 * i] + Gl[i + n1 * i];
-  const double norm2 = block_sum(loc, sh + 8);
+  for (int i = threadIdx.x; i < d1; i += NT) loc += G[i + d1 * i] + Gl[i + d1 * i];
+  const double trace = block_sum(loc, sh + 8);
+  double norm2 = trace;
+  int k1 = 0;
+  if (wroute && trace > 0.0 && isfinite(trace)) {
+    k1 = chol_piv_dd(G, Gl, d1, 1e-31 * trace, Rc, D, piv, sh);
+    // M = C^T (k1 x n1, ld D1) into Tb: M(r, i) = sum_{v >= r} R_W(r, v) F(i, piv[v])
+    double l2 = 0.0;
+    for2d(k1, n1, [&](int r, int i) {
+      double s = 0.0;
+      for (int v = r; v < d1; ++v) s += Rc[r + D * v] * F[i + n1 * piv[v]];
+      Tb[r + D1 * i] = s;
+      l2 += s * s;
+    });
+    norm2 = block_sum(l2, sh + 8);
+  }
   if (norm2 == 0.0 || !isfinite(norm2)) {
     // canonical zero, TtTensor::constant(n1, n2, n3, 0) (reference :168)
     if (threadIdx.x == 0) {
@@ -940,10 +978,16 @@ __global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
   const double budget2 = p.eps * p.eps * norm2 / 2.0;
   const double cthresh = 1e-31 * norm2;
   const SvdWork sw{p.prof, Xs, vn, sig, sraw, piv, perm, sh, mx};
-  const int k1 = chol_piv_dd(G, Gl, n1, cthresh, Rc, mx, piv, sh);
-  PROF(3);
   double mg1 = 0.0;
-  const int t1 = svd_from_r(Rc, mx, k1, n1, piv, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
+  int t1;
+  if (wroute) {
+    PROF(3);
+    t1 = svd_left(Tb, D1, k1, n1, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
+  } else {
+    k1 = chol_piv_dd(G, Gl, n1, cthresh, Rc, D, piv, sh);
+    PROF(3);
+    t1 = svd_from_r(Rc, D, k1, n1, piv, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
+  }
   if (p.margins && threadIdx.x == 0) p.margins[2 * o] = mg1;
   PROF(5);
   for2d(t1, R1, [&](int r, int col) {  // P = U1^T F
@@ -978,11 +1022,11 @@ __global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
   gram_store<Q>(G, Gl, q3, gh, gl, ei, ej);
   __syncthreads();
   PROF(6);
-  const int k2 = chol_piv_dd(G, Gl, q3, cthresh, Rc, mx, piv, sh);
+  const int k2 = chol_piv_dd(G, Gl, q3, cthresh, Rc, D, piv, sh);
   PROF(7);
   double mg2 = 0.0;
-  double* W2 = Tb;  // V2 (q3 x t2), ld mx
-  const int t2 = svd_from_r(Rc, mx, k2, q3, piv, sw, budget2, p.cap, W2, mx, &mg2, &s_meta[5]);
+  double* W2 = Tb;  // V2 (q3 x t2), ld D3
+  const int t2 = svd_from_r(Rc, D, k2, q3, piv, sw, budget2, p.cap, W2, D3, &mg2, &s_meta[5]);
   PROF(9);
   if (threadIdx.x == 0) {
     if (p.margins) p.margins[2 * o + 1] = mg2;
@@ -1015,14 +1059,14 @@ __global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
   double* dmid = dst + (long long)n1 * t1;
   double* dlast = dmid + (long long)n2 * t1 * t2;
   for (int e = threadIdx.x; e < n1 * t1; e += NT) dst[e] = U1[e];
-  // G = [W2; 0] (n3 x t2) into Xs; Z = R3^T W2 (R2 x t2, ld ZR) into the Gram region
-  for2d(n3, t2, [&](int c, int s) { Xs[c + mx * s] = c < q3 ? W2[c + mx * s] : 0.0; });
+  // G = [W2; 0] (n3 x t2) into Xs; Z = R3^T W2 (R2 x t2, ld RM2) into the Gram region
+  for2d(n3, t2, [&](int c, int s) { Xs[c + mx * s] = c < q3 ? W2[c + D3 * s] : 0.0; });
   double* Z = G;
   for2d(R2, t2, [&](int b, int s) {
     double acc = 0.0;
     const int cm = min(b, q3 - 1);
-    for (int c = 0; c <= cm; ++c) acc += lastT[c + n3 * b] * W2[c + mx * s];
-    Z[b + ZR * s] = acc;
+    for (int c = 0; c <= cm; ++c) acc += lastT[c + n3 * b] * W2[c + D3 * s];
+    Z[b + RM2 * s] = acc;
   });
   __syncthreads();
   const int kmax = min(n3, R2);
@@ -1050,10 +1094,10 @@ __global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
       double a0 = 0.0, a1 = 0.0;
       int b = 0;
       for (; b + 1 < R2; b += 2) {
-        a0 += X2[r + n1 * b] * Z[b + ZR * s];
-        a1 += X2[r + n1 * (b + 1)] * Z[b + 1 + ZR * s];
+        a0 += X2[r + n1 * b] * Z[b + RM2 * s];
+        a1 += X2[r + n1 * (b + 1)] * Z[b + 1 + RM2 * s];
       }
-      if (b < R2) a0 += X2[r + n1 * b] * Z[b + ZR * s];
+      if (b < R2) a0 += X2[r + n1 * b] * Z[b + RM2 * s];
       dmid[(long long)j * t1 * t2 + r + t1 * s] = a0 + a1;
     });
   }
@@ -1065,25 +1109,30 @@ __global__ void __launch_bounds__(NT, 3) round_gram_kernel(RoundArgs p) {
 size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX) {
   const size_t mx = n1 > n3 ? n1 : n3;
   const size_t RMX = RM1 > RM2 ? RM1 : RM2;
-  const size_t ZR = (2 * mx > (size_t)RM2) ? 2 * mx : RM2;
-  size_t d = (size_t)n1 * RMX + (size_t)n3 * RM2 + mx + mx * mx + ZR * mx + (size_t)n1 * RMX +
-             (size_t)n1 * n1 + 2 * mx * mx + (size_t)MSMAX + 3 * mx + 32;
+  const size_t D1 = n1 < RM1 ? n1 : RM1, D3 = n3 < RM2 ? n3 : RM2;
+  const size_t D = D1 > D3 ? D1 : D3;
+  const size_t GZ = 2 * D * D > (size_t)RM2 * D ? 2 * D * D : (size_t)RM2 * D;
+  size_t d = (size_t)n1 * RMX + (size_t)n3 * RM2 + mx + mx * D + GZ + (size_t)n1 * RMX +
+             (size_t)n1 * D1 + mx * D + D * D + (size_t)MSMAX + 3 * mx + 32;
   size_t ints = 2 * mx + RM2 + RM1 + 1;
   return d * 8 + ((ints * 4 + 7) / 8) * 8 + sizeof(TermInfo) * kMaxTerms + 64;
 }
 
-cudaError_t launch_round_gram(const RoundArgs& a, cudaStream_t st) {
-  if (a.nout == 0) return cudaSuccess;
+cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st) {
+  if (nblocks == 0) return cudaSuccess;
   const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX);
-  const int mx = a.n1 > a.n3 ? a.n1 : a.n3;
-  const int ne = mx * (mx + 1) / 2;
+  const int D1 = a.n1 < a.RM1 ? a.n1 : a.RM1, D3 = a.n3 < a.RM2 ? a.n3 : a.RM2;
+  const int D = D1 > D3 ? D1 : D3;
+  const int ne = D * (D + 1) / 2;
   cudaError_t e = cudaSuccess;
 #define LAUNCH_Q(QV)                                                                          \
   e = cudaFuncSetAttribute(round_gram_kernel<QV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)smem);                                                         \
   if (e != cudaSuccess) return e;                                                              \
-  round_gram_kernel<QV><<<a.nout, NT, smem, st>>>(a);
-  if (ne <= 3 * NT) {
+  round_gram_kernel<QV><<<nblocks, NT, smem, st>>>(a);
+  if (ne <= NT) {
+    LAUNCH_Q(1)
+  } else if (ne <= 3 * NT) {
     LAUNCH_Q(3)
   } else if (ne <= 5 * NT) {
     LAUNCH_Q(5)
@@ -1110,8 +1159,13 @@ size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int 
   return bytes;
 }
 
-// Per-launch bounds: max over outputs of summed ranks, middle sizes, terms.
-__global__ void round_bounds_kernel(RoundArgs p, int* bounds) {
+// Rank bins (SURVEY.md §7 hard part 3): outputs are grouped by the largest
+// summed rank max(R1, R2) so that each launch's shared-memory plan -- and
+// with it the CTAs per SM -- fits its own outputs.  bins[b] lists the
+// outputs with kRankEdges[b-1] < key <= kRankEdges[b]; bmax[4 b + {0,1,2}]
+// are the bin's RM1, RM2, MSMAX.  Order inside a bin is nondeterministic;
+// every output is computed independently, so results are not.
+__global__ void round_bin_kernel(RoundArgs p, int* counts, int* bmax, int* lists) {
   for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < p.nout; o += gridDim.x * blockDim.x) {
     const long long t0 = p.term_off ? p.term_off[o] : o;
     const int K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
@@ -1128,17 +1182,23 @@ __global__ void round_bounds_kernel(RoundArgs p, int* bounds) {
       r2 += b;
       ms += a * b;
     }
-    atomicMax(&bounds[0], r1);
-    atomicMax(&bounds[1], r2);
-    atomicMax(&bounds[2], ms);
-    atomicMax(&bounds[3], K);
+    const int key = max(r1, r2);
+    int bin = 0;
+    while (bin < kRankBins - 1 && key > kRankEdges[bin]) ++bin;
+    const int pos = atomicAdd(&counts[bin], 1);
+    lists[(long long)bin * p.nout + pos] = o;
+    atomicMax(&bmax[4 * bin], r1);
+    atomicMax(&bmax[4 * bin + 1], r2);
+    atomicMax(&bmax[4 * bin + 2], ms);
+    atomicMax(&bmax[4 * bin + 3], K);
   }
 }
 
-cudaError_t launch_round_bounds(const RoundArgs& a, int* bounds, cudaStream_t st) {
+cudaError_t launch_round_bins(const RoundArgs& a, int* counts, int* bmax, int* lists,
+                              cudaStream_t st) {
   if (a.nout == 0) return cudaSuccess;
   const int blocks = min(1184, (a.nout + 255) / 256);
-  round_bounds_kernel<<<blocks, 256, 0, st>>>(a, bounds);
+  round_bin_kernel<<<blocks, 256, 0, st>>>(a, counts, bmax, lists);
   return cudaGetLastError();
 }
 

@@ -9,6 +9,10 @@ namespace ttdvm {
 constexpr int kMaxSets = 12;
 constexpr int kMaxTerms = 16;     // summands per rounded output
 constexpr int kRoundThreads = 128;
+// rank bins of a rounding launch: upper edges of max(R1, R2) of the summed input
+constexpr int kRankBins = 11;
+__device__ __constant__ const int kRankEdges[kRankBins] = {4, 8, 12, 16, 24, 32, 48, 64, 96, 128,
+                                                           1 << 30};
 
 // A set of packed TT tensors (ttdvm_tt_batch layout) resident in an arena.
 struct TSet {
@@ -72,6 +76,7 @@ struct RoundArgs {
   const Term* terms;
   const double* factors;        // [nfac][n1+n2+n3]
   const double* dscale;         // per-step device scales (Term::dsi)
+  const int* olist;             // optional: block b rounds output olist[b] (rank bins)
   int n1, n2, n3;
   int nout;
   double eps;
