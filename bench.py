@@ -1,19 +1,25 @@
 #!/usr/bin/env python
-"""Benchmark of the TT-DVM explicit step (BASELINE.json metric: cell-steps/s).
+"""Benchmark of the TT-DVM explicit step (BASELINE.json metric: cell-steps/s
+at the 44^3 velocity mesh).
 
 A "step" is one explicit step S1 over every cell of the
 workload's mesh, with the state resident in HBM.  Default workload: config
-2 of BASELINE.json (32^3 periodic hex cells, 24^3 velocity mesh, eps 1e-6,
-seeded synthetic smooth Maxwellian fields + a rank-2 perturbation); see
-DESIGN.md for why config 4 (44^3) is not yet the N=1 workload.
+4 of BASELINE.json -- the unstructured (jittered, shuffled) hex mesh of
+511,488 cells around an 8^3 obstacle, 44^3 velocity mesh on [-7,7]^3, Mach-3
+free stream, diffuse walls, eps 1e-5, fp64 (synthetic, seeded).  The
+one-time face-factor set-up (|xi_n| estimates of 1.5 M distinct oblique
+normals) is timed separately (config.setup_s), not inside the step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1|2|4|5] [--scale s]
 
-N > 1 under torchrun: every rank steps its own full copy of the workload
-("replicas", weak scaling) until the slab partition's halo exchange lands;
-the timing is the max over ranks of the CUDA-event time of the K steps.
---impl reference times the CPU oracle (the numpy restatement of the
-reference, all host cores, one process per core) on a bounded sample.
+N > 1 under torchrun: config 4 is partitioned by recursive coordinate
+bisection of the cell centroids (strong scaling, the same mesh on N GPUs);
+configs 2 / 5 stack N x-slabs of the single-GPU box (weak scaling).  Halo TT
+cores of cut faces are exchanged every step over NCCL.  The timing is the
+max over ranks of the CUDA-event time of the K steps.  --impl reference
+times the CPU oracle (the numpy restatement of the reference, all host
+cores, one process per core) on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -38,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
@@ -49,7 +55,7 @@ def workload_config(p, args):
     return {"workload": p.name, "config_index": args.config, "cells": int(p.mesh.ncell),
             "faces": int(p.mesh.nface), "velocity_mesh": f"{p.nv}^3 on [-{p.bound},{p.bound}]^3",
             "eps": p.eps, "rank_cap": p.cap, "dt": p.dt,
-            "l2_policy": "inputs larger than L2 (state arena >> 126 MB)",
+            "l2_policy": "inputs larger than L2 (state and face-factor arenas >> 126 MB)",
             "timed_from": "initial state re-uploaded after warm-up (steps 1..K of the run)"}
 
 
@@ -154,7 +160,7 @@ def cpu_oracle_rate(cfg, scale, ncells: int, workers: int, repeats: int = 1):
     ctxm = mp.get_context("spawn")
     times = []
     with ctxm.Pool(workers, initializer=_ref_worker_init, initargs=((cfg, scale),)) as pool:
-        pool.map(_ref_task, [[0]] * workers)  # warm imports
+        pool.map(_ref_task, strips)  # warm: imports and the strips' face factors
         for _ in range(repeats):
             t = time.perf_counter()
             pool.map(_ref_task, strips)
@@ -217,20 +223,32 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1912_04582_b200.cuda import Context
     from paper_1912_04582_b200.problems import config
+    t_setup = time.perf_counter()
     p = config(args.config, args.scale)
+    setup = {"mesh_and_state_s": round(time.perf_counter() - t_setup, 2)}
     ctx = Context(local)
     part = None
+    scaling = "weak"
+    ncell_total = p.mesh.ncell
     if world > 1:
-        # weak scaling: the global periodic box is `world` x-slabs of the
-        # single-GPU workload; each rank owns one slab plus its halo ghosts
         from paper_1912_04582_b200 import halo
         from paper_1912_04582_b200.partition import build_part, local_state
-        from paper_1912_04582_b200.problems import periodic_box
-        nx, ny, nz = p.mesh.shape
-        pg = periodic_box((nx * world, ny, nz), nv=p.nv, bound=p.bound, eps=p.eps, cap=p.cap,
-                          name=p.name + f"-x{world}")
-        from paper_1912_04582_b200.mesh import slab_partition
-        part = build_part(pg.mesh, slab_partition(pg.mesh, world), rank)
+        if args.config == 4:
+            # strong scaling: one mesh, RCB of the cell centroids over the ranks
+            from paper_1912_04582_b200.mesh import rcb_partition
+            part = build_part(p.mesh, rcb_partition(p.mesh.centroids, world), rank)
+            scaling = "strong"
+            pg = p
+        else:
+            # weak scaling: the global periodic box is `world` x-slabs of the
+            # single-GPU workload; each rank owns one slab plus its halo ghosts
+            from paper_1912_04582_b200.mesh import slab_partition
+            from paper_1912_04582_b200.problems import periodic_box
+            nx, ny, nz = p.mesh.shape
+            pg = periodic_box((nx * world, ny, nz), nv=p.nv, bound=p.bound, eps=p.eps, cap=p.cap,
+                              name=p.name + f"-x{world}")
+            part = build_part(pg.mesh, slab_partition(pg.mesh, world), rank)
+            ncell_total = pg.mesh.ncell
         ctx.set_grid(pg.nv, pg.bound)
         ctx.set_gas(pg.gas)
         ctx.set_mesh(part.mesh)
@@ -245,6 +263,10 @@ def main():
         ctx.setup(p)
         f_local = p.f0
         cells_per_rank = p.mesh.ncell
+    t0 = time.perf_counter()
+    ctx.step(p.dt, p.eps, p.cap, 0)  # face factors, wall set-up, summand lists
+    setup["face_factors_s"] = round(time.perf_counter() - t0, 2)
+    setup.update({k: v for k, v in ctx.setup_info().items() if k != "face_factor_ms"})
     fp64_peak = ctx.fp64_peak()
 
     def run_steps(k):
@@ -279,8 +301,7 @@ def main():
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    cells = cells_per_rank
-    value = world * cells * args.steps / (ms / 1e3)
+    value = ncell_total * args.steps / (ms / 1e3)
 
     # e2e through the public API with host buffers: upload state, one step,
     # download state -- every step
@@ -307,7 +328,7 @@ def main():
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = world * cells * args.e2e_steps / e2e_s
+    e2e_value = ncell_total * args.e2e_steps / e2e_s
 
     # roofline of the dominant kernel (the rounding phase with most time)
     names = ["moments", "shakhov_build", "round_fs", "round_collision", "round_flux",
@@ -316,7 +337,7 @@ def main():
     dom_s = phase_ms[dom] / 1e3
     achieved = flops[dom] / dom_s / 1e12 if dom_s > 0 else 0.0
     traffic = traffic_from_profiles().get(names[dom])
-    roofline = {"bound": "fp64", "kernel": f"round_sums_kernel ({names[dom]})",
+    roofline = {"bound": "fp64", "kernel": f"round_gram_kernel ({names[dom]})",
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak if fp64_peak else None,
                 "peak_source": "measured on this GPU by the DFMA probe in libttdvm_cuda.so",
@@ -339,13 +360,15 @@ def main():
     if rank == 0:
         line = {"metric": "cell-steps/s", "value": value, "unit": "cell-steps/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": dict(workload_config(p, args),
-                                                    parallelism=(f"x-slab partition x{world}, "
-                                                                 "halo TT cores over NCCL"
-                                                                 if world > 1 else "single GPU"),
-                                                    cells_per_gpu=cells_per_rank,
-                                                    max_rank_after=max_rank),
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": dict(workload_config(p, args),
+                               parallelism=((f"RCB partition x{world}" if args.config == 4 else
+                                             f"x-slab partition x{world}") +
+                                            ", halo TT cores over NCCL" if world > 1
+                                            else "single GPU"),
+                               cells_total=ncell_total, cells_per_gpu=cells_per_rank,
+                               max_rank_after=max_rank, setup_s=setup),
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "cell-steps/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "steps": args.e2e_steps},

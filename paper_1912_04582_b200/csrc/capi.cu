@@ -29,7 +29,7 @@ cudaError_t launch_round(const RoundArgs& a, cudaStream_t st);
 cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_round_bins(const RoundArgs& a, int* counts, int* bmax, int* lists,
                               cudaStream_t st);
-size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX);
+size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX, int JB);
 size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int MSMAX);
 struct MacroArgs {
   TSet set;
@@ -410,14 +410,28 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
       throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory"};
   }
   struct Launch {
-    int bin, count, rm1, rm2, ms;
+    int bin, count, rm1, rm2, ms, jb;
+  };
+  // slices per barrier phase: as many as fit the shared memory that the
+  // kernel variant's register-limited occupancy leaves per CTA
+  auto pick_jb = [&](int rm1, int rm2, int ms) {
+    const int D = std::max(std::min(n, rm1), std::min(n, rm2));
+    const int ne = D * (D + 1) / 2;
+    const int minb = ne <= kRoundThreads ? 6 : (ne <= 3 * kRoundThreads ? 4 : 3);
+    const size_t base = round_gram_smem_bytes(n, n, rm1, rm2, ms, 1);
+    const size_t budget = std::max(base, (size_t)(228 * 1024 / minb) - 2048);
+    int jb = 1;
+    for (int cand = 2; cand <= n; ++cand)
+      if (round_gram_smem_bytes(n, n, rm1, rm2, ms, cand) <= budget) jb = cand;
+    return jb;
   };
   std::vector<Launch> plan;
   for (int b = kRankBins - 1; b >= 0; --b) {  // large ranks first (long CTAs start early)
     if (!bcount[b]) continue;
-    const Launch l{b, bcount[b], std::max(1, bmax[4 * b]), std::max(1, bmax[4 * b + 1]),
-                   std::max(1, bmax[4 * b + 2])};
-    if (!use_tsqr && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms) > 227 * 1024)
+    Launch l{b, bcount[b], std::max(1, bmax[4 * b]), std::max(1, bmax[4 * b + 1]),
+             std::max(1, bmax[4 * b + 2]), 1};
+    l.jb = use_tsqr ? 1 : pick_jb(l.rm1, l.rm2, l.ms);
+    if (!use_tsqr && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1) > 227 * 1024)
       throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory (n=" +
                                    std::to_string(n) + ", summed ranks " +
                                    std::to_string(l.rm1) + "x" + std::to_string(l.rm2) + ")"};
@@ -450,6 +464,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
         a.RM1 = l.rm1;
         a.RM2 = l.rm2;
         a.MSMAX = l.ms;
+        a.JB = l.jb;
         a.olist = c->d_olist.p + (size_t)l.bin * nout;
         CK(launch_round_gram(a, l.count, c->st));
         c->launches += 1;

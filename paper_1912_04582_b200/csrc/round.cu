@@ -527,6 +527,89 @@ __device__ void times_r3t(double* out, int ldo, bool trans, const double* X, int
 
 // Gram accumulation of the rows of T (rows x ncol, ld ldt) into the
 // register-resident upper-triangle entries (ei, ej) of this thread.
+// ---- slice-batched helpers of the exact-Gram kernel: jn consecutive
+// slices j0 .. j0 + jn - 1 per call, flattened over (slice, element) so all
+// threads stay busy when the per-slice blocks are small ----
+__device__ void stage_slices(double* Ms, int msld, const TermInfo* terms, int K, int n1, int n2,
+                             int j0, int jn) {
+  for (int k = 0; k < K; ++k) {
+    const TermInfo& t = terms[k];
+    const int sz = t.r1 * t.r2;
+    for (int e = threadIdx.x; e < jn * sz; e += NT) {
+      const int jj = e / sz, r = e - jj * sz;
+      const int j = j0 + jj;
+      const int jr = t.refl == 2 ? n2 - 1 - j : j;
+      const double* src = t.base + (long long)n1 * t.b1 + (long long)jr * t.b1 * t.b2;
+      const double f = t.u[1] ? t.u[1][j] : 1.0;
+      double v;
+      if (!t.fb) {
+        v = f * src[r];
+      } else {  // Kronecker block A2_j (x) B2_j: (p*b1 + q, p'*b2 + q') = A(p,p') B(q,q')
+        const double* fs = t.fb + (long long)n1 * t.fa1 + (long long)j * t.fa1 * t.fa2;
+        const int c = r / t.r1, a = r - c * t.r1;
+        const int p = a / t.b1, q = a - p * t.b1;
+        const int pp = c / t.b2, qq = c - pp * t.b2;
+        v = f * fs[p + t.fa1 * pp] * src[q + t.b1 * qq];
+      }
+      Ms[jj * msld + t.ms + r] = v;
+    }
+  }
+}
+
+// X_jj (rows x R2, ld ldx, slice stride xs) = L (rows x R1, ld ldl) blockdiag(Ms_jj)
+__device__ void left_times_blockdiag_b(double* X, int ldx, int xs, const double* L, int ldl,
+                                       int rows, int R2, const double* Ms, int msld,
+                                       const TermInfo* terms, const int* colterm, int jn) {
+  const int ngr = (rows + 3) >> 2;
+  for2d(ngr, jn * R2, [&](int ig, int jc) {
+    const int jj = jc / R2, col = jc - jj * R2;
+    const int i0 = ig << 2;
+    const TermInfo& t = terms[colterm[col]];
+    const double* mcol = Ms + jj * msld + t.ms + t.r1 * (col - t.off2);
+    const double* lr = L + ldl * t.off1;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int a = 0; a < t.r1; ++a) {
+      const double m = mcol[a];
+      const double* l = lr + ldl * a + i0;
+      a0 += l[0] * m;
+      if (i0 + 1 < rows) a1 += l[1] * m;
+      if (i0 + 2 < rows) a2 += l[2] * m;
+      if (i0 + 3 < rows) a3 += l[3] * m;
+    }
+    double* xo = X + jj * xs + ldx * col + i0;
+    xo[0] = a0;
+    if (i0 + 1 < rows) xo[1] = a1;
+    if (i0 + 2 < rows) xo[2] = a2;
+    if (i0 + 3 < rows) xo[3] = a3;
+  });
+}
+
+// out_jj(c, r) = sum_{b >= c} X_jj(r, b) R3(c, b) (transposed, ld ldo, slice
+// stride os) for r < rows, c < ncol; X_jj at X + jj * xs (ld ldx)
+__device__ void times_r3t_b(double* out, int ldo, int os, const double* X, int ldx, int xs,
+                            int rows, int ncol, int R2, const double* lastT, int n3, int jn) {
+  const int ngr = (rows + 3) >> 2;
+  for2d(ngr, jn * ncol, [&](int ig, int jc) {
+    const int jj = jc / ncol, c = jc - jj * ncol;
+    const int r0 = ig << 2;
+    const double* xb = X + jj * xs + r0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int b = c; b < R2; ++b) {
+      const double l = lastT[c + n3 * b];
+      const double* xp = xb + ldx * b;
+      a0 += xp[0] * l;
+      if (r0 + 1 < rows) a1 += xp[1] * l;
+      if (r0 + 2 < rows) a2 += xp[2] * l;
+      if (r0 + 3 < rows) a3 += xp[3] * l;
+    }
+    double* o = out + jj * os + c;
+    o[ldo * r0] = a0;
+    if (r0 + 1 < rows) o[ldo * (r0 + 1)] = a1;
+    if (r0 + 2 < rows) o[ldo * (r0 + 2)] = a2;
+    if (r0 + 3 < rows) o[ldo * (r0 + 3)] = a3;
+  });
+}
+
 template <int Q>
 __device__ __forceinline__ void gram_rows_acc(double (&gh)[Q], double (&gl)[Q], const int (&ei)[Q],
                                               const int (&ej)[Q], const double* T, int ldt,
@@ -843,18 +926,23 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
   // low-rank sums (the rank bins of run_round) fit several CTAs per SM.
   const int D1 = min(n1, RM1), D3 = min(n3, RM2), D = max(D1, D3);
   const int GZ = max(2 * D * D, RM2 * D);
-  double* F = sm;                          // n1 x RMX   (cut 2 / output: X2)
+  // JB slices per barrier phase in the W route, cut 2 and the output (the
+  // T route stages one slice at a time); chosen by the host from the budget
+  const int JB = p.JB;
+  const int TBZ = max(mx * D, JB * D1 * D3);
+  double* F = sm;                          // n1 x RMX   (cut 2 / output: X2 when JB = 1)
   double* lastT = F + n1 * RMX;            // n3 x RM2
   double* tau = lastT + n3 * RM2;          // mx
-  double* Tb = tau + mx;                   // mx x D     (slice blocks, C^T; V2 at the end)
-  double* G = Tb + mx * D;                 // GZ         (Gram hi/lo planes; Z at the end)
+  double* Tb = tau + mx;                   // TBZ        (slice blocks, C^T; V2 at the end)
+  double* G = Tb + TBZ;                    // GZ         (Gram hi/lo planes; Z at the end)
   double* Gl = G + D * D;
   double* XP = G + GZ;                     // n1 x RMX   (cut 1: X; cut 2: P)
   double* U1 = XP + n1 * RMX;              // n1 x D1
   double* Xs = U1 + n1 * D1;               // mx x D     (Jacobi workspace)
   double* Rc = Xs + mx * D;                // D x D      (Cholesky factor)
-  double* Ms = Rc + D * D;                 // p.MSMAX
-  double* sig = Ms + p.MSMAX;              // mx
+  double* Ms = Rc + D * D;                 // JB x p.MSMAX (staged middle slices)
+  double* X2c = Ms + JB * p.MSMAX;         // JB x D1 x RMX when JB > 1 (P M_j per slice)
+  double* sig = X2c + (JB > 1 ? JB * D1 * RMX : 0);  // mx
   double* sraw = sig + mx;                 // mx
   double* vn = sraw + mx;                  // mx
   double* sh = vn + mx;                    // 32 scalars
@@ -905,27 +993,36 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
       else ei[q] = ej[q] = -1;
     }
   }
-  for (int j = 0; j < n2; ++j) {
-    __syncthreads();
-    stage_slice(Ms, terms, K, n1, n2, j);
-    __syncthreads();
-    if (wroute) {
-      // Z_j^T: Tb(a, c) = sum_b M_t(a, b) R3(c, off2 + b), R3 upper trapezoidal
-      for2d(R1, q3, [&](int a, int c) {
+  if (wroute) {
+    for (int j0 = 0; j0 < n2; j0 += JB) {
+      const int jn = min(JB, n2 - j0);
+      __syncthreads();
+      stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
+      __syncthreads();
+      // Z_j^T: Tb(a, (jj, c)) = sum_b M_t(a, b) R3(c, off2 + b), R3 upper trapezoidal
+      for2d(R1, jn * q3, [&](int a, int jc) {
+        const int jj = jc / q3, c = jc - jj * q3;
         const TermInfo& t = terms[rowterm[a]];
         const int aa = a - t.off1;
+        const double* mj = Ms + jj * p.MSMAX + t.ms + aa;
         double s = 0.0;
-        for (int b = max(0, c - t.off2); b < t.r2; ++b)
-          s += lastT[c + n3 * (t.off2 + b)] * Ms[t.ms + aa + t.r1 * b];
-        Tb[a + d1 * c] = s;
+        for (int b = max(0, c - t.off2); b < t.r2; ++b) s += lastT[c + n3 * (t.off2 + b)] * mj[t.r1 * b];
+        Tb[a + d1 * jc] = s;
       });
-    } else {
+      __syncthreads();
+      gram_rows_acc<Q>(gh, gl, ei, ej, Tb, d1, jn * q3);
+    }
+  } else {
+    for (int j = 0; j < n2; ++j) {
+      __syncthreads();
+      stage_slice(Ms, terms, K, n1, n2, j);
+      __syncthreads();
       left_times_blockdiag(XP, n1, F, n1, n1, R2, Ms, terms, colterm);
       __syncthreads();
       times_r3t(Tb, n1, false, XP, n1, n1, q3, R2, lastT, n3);
+      __syncthreads();
+      gram_rows_acc<Q>(gh, gl, ei, ej, Tb, d1, q3);
     }
-    __syncthreads();
-    gram_rows_acc<Q>(gh, gl, ei, ej, Tb, d1, q3);
   }
   __syncthreads();
   gram_store<Q>(G, Gl, d1, gh, gl, ei, ej);
@@ -997,7 +1094,6 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
   });
 
   // ---- cut 2: G2 = sum_j S_j^T S_j (q3 x q3), S_j = P M_j R3^T ----
-  double* X2 = F;
   {
     const int ne = q3 * (q3 + 1) / 2;
 #pragma unroll
@@ -1008,15 +1104,19 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
       else ei[q] = ej[q] = -1;
     }
   }
-  for (int j = 0; j < n2; ++j) {
+  // X2_j = P blockdiag(M_j) (t1 x R2, ld t1), JB slices per phase
+  double* X2 = JB > 1 ? X2c : F;
+  for (int j0 = 0; j0 < n2; j0 += JB) {
+    const int jn = min(JB, n2 - j0);
     __syncthreads();
-    stage_slice(Ms, terms, K, n1, n2, j);
+    stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
     __syncthreads();
-    left_times_blockdiag(X2, n1, XP, n1, t1, R2, Ms, terms, colterm);
+    left_times_blockdiag_b(X2, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn);
     __syncthreads();
-    times_r3t(Tb, q3, true, X2, n1, t1, q3, R2, lastT, n3);  // S_j^T (q3 x t1)
+    // S_j^T (q3 x t1) at column block jj
+    times_r3t_b(Tb, q3, q3 * t1, X2, t1, t1 * R2, t1, q3, R2, lastT, n3, jn);
     __syncthreads();
-    gram_rows_acc<Q>(gh, gl, ei, ej, Tb, q3, t1);
+    gram_rows_acc<Q>(gh, gl, ei, ej, Tb, q3, jn * t1);
   }
   __syncthreads();
   gram_store<Q>(G, Gl, q3, gh, gl, ei, ej);
@@ -1084,21 +1184,26 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
   }
   __syncthreads();
   for2d(t2, n3, [&](int s, int kk) { dlast[s + t2 * kk] = Xs[kk + mx * s]; });
-  for (int j = 0; j < n2; ++j) {
+  for (int j0 = 0; j0 < n2; j0 += JB) {
+    const int jn = min(JB, n2 - j0);
     __syncthreads();
-    stage_slice(Ms, terms, K, n1, n2, j);
+    stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
     __syncthreads();
-    left_times_blockdiag(X2, n1, XP, n1, t1, R2, Ms, terms, colterm);
+    left_times_blockdiag_b(X2, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn);
     __syncthreads();
-    for2d(t1, t2, [&](int r, int s) {
+    // middle_j = (P blockdiag(M_j)) Z
+    for2d(t1, jn * t2, [&](int r, int js) {
+      const int jj = js / t2, s = js - jj * t2;
+      const double* x = X2 + jj * t1 * R2 + r;
+      const double* z = Z + RM2 * s;
       double a0 = 0.0, a1 = 0.0;
       int b = 0;
       for (; b + 1 < R2; b += 2) {
-        a0 += X2[r + n1 * b] * Z[b + RM2 * s];
-        a1 += X2[r + n1 * (b + 1)] * Z[b + 1 + RM2 * s];
+        a0 += x[t1 * b] * z[b];
+        a1 += x[t1 * (b + 1)] * z[b + 1];
       }
-      if (b < R2) a0 += X2[r + n1 * b] * Z[b + RM2 * s];
-      dmid[(long long)j * t1 * t2 + r + t1 * s] = a0 + a1;
+      if (b < R2) a0 += x[t1 * b] * z[b];
+      dmid[(long long)(j0 + jj) * t1 * t2 + r + t1 * s] = a0 + a1;
     });
   }
   __syncthreads();
@@ -1106,21 +1211,23 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
 #undef PROF
 }
 
-size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX) {
+size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX, int JB) {
   const size_t mx = n1 > n3 ? n1 : n3;
   const size_t RMX = RM1 > RM2 ? RM1 : RM2;
   const size_t D1 = n1 < RM1 ? n1 : RM1, D3 = n3 < RM2 ? n3 : RM2;
   const size_t D = D1 > D3 ? D1 : D3;
   const size_t GZ = 2 * D * D > (size_t)RM2 * D ? 2 * D * D : (size_t)RM2 * D;
-  size_t d = (size_t)n1 * RMX + (size_t)n3 * RM2 + mx + mx * D + GZ + (size_t)n1 * RMX +
-             (size_t)n1 * D1 + mx * D + D * D + (size_t)MSMAX + 3 * mx + 32;
+  const size_t TBZ = mx * D > JB * D1 * D3 ? mx * D : JB * D1 * D3;
+  size_t d = (size_t)n1 * RMX + (size_t)n3 * RM2 + mx + TBZ + GZ + (size_t)n1 * RMX +
+             (size_t)n1 * D1 + mx * D + D * D + (size_t)JB * MSMAX +
+             (JB > 1 ? (size_t)JB * D1 * RMX : 0) + 3 * mx + 32;
   size_t ints = 2 * mx + RM2 + RM1 + 1;
   return d * 8 + ((ints * 4 + 7) / 8) * 8 + sizeof(TermInfo) * kMaxTerms + 64;
 }
 
 cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st) {
   if (nblocks == 0) return cudaSuccess;
-  const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX);
+  const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX, a.JB);
   const int D1 = a.n1 < a.RM1 ? a.n1 : a.RM1, D3 = a.n3 < a.RM2 ? a.n3 : a.RM2;
   const int D = D1 > D3 ? D1 : D3;
   const int ne = D * (D + 1) / 2;

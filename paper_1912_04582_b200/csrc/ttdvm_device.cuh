@@ -90,6 +90,7 @@ struct RoundArgs {
   int RM1, RM2;                 // bounds on the summed input ranks
   int HMAX;                     // rows of the TSQR block buffer
   int MSMAX;                    // doubles of the staged middle slices
+  int JB;                       // slices per barrier phase (exact-Gram kernel)
 };
 
 }  // namespace ttdvm

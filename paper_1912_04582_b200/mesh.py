@@ -39,6 +39,7 @@ class Mesh:
     group_names: list = field(default_factory=list)
     shape: tuple = ()          # (nx, ny, nz) for structured meshes
     cell_ijk: np.ndarray | None = None  # int32 [ncell, 3]
+    centroids: np.ndarray | None = None  # f64 [ncell, 3] (vertex mean, mesh.cpp:124-126)
 
     def cell_faces(self, c: int):
         a, b = int(self.cell_face_off[c]), int(self.cell_face_off[c + 1])
@@ -266,7 +267,31 @@ def shuffle_faces(mesh: Mesh, rng: np.random.Generator) -> Mesh:
     return Mesh(mesh.ncell, mesh.nface, mesh.face_left[perm], mesh.face_right[perm],
                 mesh.face_group[perm], mesh.face_area[perm], mesh.face_normal[perm],
                 mesh.cell_volume, mesh.cell_face_off, inv[mesh.cell_face_id].astype(np.int32),
-                mesh.cell_face_sign, mesh.group_names, mesh.shape, mesh.cell_ijk)
+                mesh.cell_face_sign, mesh.group_names, mesh.shape, mesh.cell_ijk,
+                mesh.centroids)
+
+
+def rcb_partition(points: np.ndarray, nparts: int) -> np.ndarray:
+    """Recursive coordinate bisection: split the
+    point set at the median of its longest extent, recursively, into nparts
+    (any positive count; parts differ in size by at most one point per
+    level).  Returns the owner rank per point (int32)."""
+    owner = np.zeros(points.shape[0], dtype=np.int32)
+
+    def split(idx, lo, k):
+        if k == 1:
+            owner[idx] = lo
+            return
+        kl = k // 2
+        pts = points[idx]
+        ax = int(np.argmax(pts.max(axis=0) - pts.min(axis=0)))
+        order = idx[np.argsort(pts[:, ax], kind="stable")]
+        cut = (order.shape[0] * kl) // k
+        split(order[:cut], lo, kl)
+        split(order[cut:], lo + kl, k - kl)
+
+    split(np.arange(points.shape[0]), 0, nparts)
+    return owner
 
 
 def obstacle_mesh(shape=(100, 80, 64), hole: int = 8, h: float = 1.0, jitter: float = 0.1,
@@ -315,6 +340,7 @@ def obstacle_mesh(shape=(100, 80, 64), hole: int = 8, h: float = 1.0, jitter: fl
 
     m = build_mesh(xyz, cells, groups, ("inlet", "outlet", "wall"), area="vector")
     m.cell_ijk = ijk
+    m.centroids = xyz[cells].mean(axis=1)
     m.shape = tuple(shape)
     if shuffle:
         m = shuffle_faces(m, rng)

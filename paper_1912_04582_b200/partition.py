@@ -59,6 +59,26 @@ def build_part(mesh: Mesh, owner: np.ndarray, rank: int) -> LocalPart:
     local = _finish(int(loc.shape[0]), lf, rf, mesh.face_group[fids], mesh.face_area[fids],
                     mesh.face_normal[fids], mesh.cell_volume[loc], mesh.group_names, mesh.shape,
                     ijk)
+    if mesh.centroids is not None:
+        local.centroids = mesh.centroids[loc]
+    # owned cells keep the global (face, sign) order, so a partitioned step
+    # adds each cell's summands in the single-rank order (bit-identical sums)
+    f2l = -np.ones(mesh.nface, dtype=np.int64)
+    f2l[fids] = np.arange(fids.shape[0])
+    go = mesh.cell_face_off
+    cnt = (go[owned + 1] - go[owned]).astype(np.int64)
+    idx = np.repeat(go[owned] - np.cumsum(cnt) + cnt, cnt) + np.arange(int(cnt.sum()))
+    lo_ = local.cell_face_off
+    nown = owned.shape[0]
+    gcnt = np.diff(lo_)[nown:]
+    gidx = np.arange(int(lo_[nown]), int(lo_[-1]))
+    local.cell_face_id = np.concatenate([f2l[mesh.cell_face_id[idx]],
+                                         local.cell_face_id[gidx]]).astype(np.int32)
+    local.cell_face_sign = np.concatenate([mesh.cell_face_sign[idx],
+                                           local.cell_face_sign[gidx]]).astype(np.int8)
+    off = np.zeros(loc.shape[0] + 1, dtype=np.int64)
+    np.cumsum(np.concatenate([cnt, gcnt]), out=off[1:])
+    local.cell_face_off = off
     part = LocalPart(rank, nparts, owned, ghosts, local, fids)
     # halo plan, both directions sorted by global id (both sides agree)
     for q in range(nparts):

@@ -10,14 +10,20 @@ import pytest
 import torch
 import torch.multiprocessing as mp
 
-from paper_1912_04582_b200.mesh import slab_partition, structured_box
+from paper_1912_04582_b200.mesh import (obstacle_mesh, rcb_partition, slab_partition,
+                                        structured_box)
 from paper_1912_04582_b200.partition import build_part
 
 
-@pytest.mark.parametrize("nparts", [2, 3])
-def test_halo_plan_is_consistent(nparts):
-    mesh = structured_box(6, 3, 2, periodic=(True, True, True))
-    owner = slab_partition(mesh, nparts)
+@pytest.mark.parametrize("kind,nparts", [("slab", 2), ("slab", 3), ("rcb", 2), ("rcb", 5)])
+def test_halo_plan_is_consistent(kind, nparts):
+    if kind == "slab":
+        mesh = structured_box(6, 3, 2, periodic=(True, True, True))
+        owner = slab_partition(mesh, nparts)
+    else:  # config 4's shuffled obstacle mesh, recursive coordinate bisection
+        mesh = obstacle_mesh((8, 6, 5), hole=2, seed=3)
+        owner = rcb_partition(mesh.centroids, nparts)
+        assert np.bincount(owner).max() - np.bincount(owner).min() <= 1
     parts = [build_part(mesh, owner, r) for r in range(nparts)]
     for p in parts:
         l2g = p.local_to_global
@@ -43,7 +49,16 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, out):
+def _problem(kind):
+    from paper_1912_04582_b200.problems import obstacle_flow, periodic_box
+    if kind == "slab":
+        p = periodic_box((4, 2, 1), steps=2)
+        return p, slab_partition(p.mesh, 2)
+    p = obstacle_flow((4, 3, 3), hole=1, nv=8, seed=5)
+    return p, rcb_partition(p.mesh.centroids, 2)
+
+
+def _worker(rank, world, port, out, kind):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch.distributed as dist
@@ -51,11 +66,9 @@ def _worker(rank, world, port, out):
     from oracle.step import OracleSolver
     from oracle.tt import TtTensor
     from paper_1912_04582_b200 import halo
-    from paper_1912_04582_b200.problems import periodic_box
     from paper_1912_04582_b200.tt_batch import TtBatch
 
-    p = periodic_box((4, 2, 1), steps=2)
-    owner = slab_partition(p.mesh, world)
+    p, owner = _problem(kind)
     part = build_part(p.mesh, owner, rank)
     solver = OracleSolver(part.mesh, p.nv, p.bound, p.gas, p.bcs)
     f = [TtTensor(*p.f0.get(int(g))) for g in part.local_to_global]
@@ -77,17 +90,17 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_gloo_two_ranks_match_single_rank():
+@pytest.mark.parametrize("kind", ["slab", "rcb"])
+def test_gloo_two_ranks_match_single_rank(kind):
     from oracle.step import OracleSolver
     from oracle.tt import TtTensor, rel_err
-    from paper_1912_04582_b200.problems import periodic_box
 
     world = 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), out, kind), nprocs=world, join=True,
                        start_method="spawn")
-    p = periodic_box((4, 2, 1), steps=2)
+    p, _ = _problem(kind)
     solver = OracleSolver(p.mesh, p.nv, p.bound, p.gas, p.bcs)
     f = [TtTensor(*p.f0.get(i)) for i in range(p.mesh.ncell)]
     for _ in range(2):
