@@ -345,7 +345,7 @@ void upload_batch(ttdvm_ctx* c, const ttdvm_tt_batch* b, TensorSet& s) {
 
 void ensure_static(ttdvm_ctx* c) {
   if (c->d_status.p == nullptr) {
-    c->d_acc.alloc(2);
+    c->d_acc.alloc(2 * kAccSlots);
     c->d_status.alloc(kStWords + 4);
     CK(cudaMallocHost(&c->h_status, 64 * sizeof(int)));
   }
@@ -412,17 +412,14 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   struct Launch {
     int bin, count, rm1, rm2, ms, jb;
   };
-  // slices per barrier phase: as many as fit the shared memory that the
-  // kernel variant's register-limited occupancy leaves per CTA
+  // slices per barrier phase: about a quarter of the slices (measured best
+  // on config 4: fewer phases pay for a lower CTA count), shrunk while the
+  // plan would leave fewer than 3 CTAs per SM
   auto pick_jb = [&](int rm1, int rm2, int ms) {
-    const int D = std::max(std::min(n, rm1), std::min(n, rm2));
-    const int ne = D * (D + 1) / 2;
-    const int minb = ne <= kRoundThreads ? 6 : (ne <= 3 * kRoundThreads ? 4 : 3);
     const size_t base = round_gram_smem_bytes(n, n, rm1, rm2, ms, 1);
-    const size_t budget = std::max(base, (size_t)(228 * 1024 / minb) - 2048);
-    int jb = 1;
-    for (int cand = 2; cand <= n; ++cand)
-      if (round_gram_smem_bytes(n, n, rm1, rm2, ms, cand) <= budget) jb = cand;
+    const size_t budget = std::max(base, (size_t)(228 * 1024 / 3) - 2048);
+    int jb = (n + 3) / 4;
+    while (jb > 1 && round_gram_smem_bytes(n, n, rm1, rm2, ms, jb) > budget) --jb;
     return jb;
   };
   std::vector<Launch> plan;
@@ -431,6 +428,14 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     Launch l{b, bcount[b], std::max(1, bmax[4 * b]), std::max(1, bmax[4 * b + 1]),
              std::max(1, bmax[4 * b + 2]), 1};
     l.jb = use_tsqr ? 1 : pick_jb(l.rm1, l.rm2, l.ms);
+    static const int force_jb = [] {  // diagnostics: TTDVM_JB=k forces k slices per phase
+      const char* e = getenv("TTDVM_JB");
+      return e ? atoi(e) : 0;
+    }();
+    if (force_jb > 0 && !use_tsqr) {
+      l.jb = std::min(n, force_jb);
+      while (l.jb > 1 && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, l.jb) > 227 * 1024) --l.jb;
+    }
     if (!use_tsqr && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1) > 227 * 1024)
       throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory (n=" +
                                    std::to_string(n) + ", summed ranks " +
@@ -451,7 +456,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     a.out.used = reinterpret_cast<unsigned long long*>(c->d_status.p + kStWords);
     a.out.capacity = (long long)out.arena.n;
     CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
-    CK(cudaMemsetAsync(c->d_acc.p, 0, 2 * sizeof(double), c->st));
+    CK(cudaMemsetAsync(c->d_acc.p, 0, 2 * kAccSlots * sizeof(double), c->st));
     if (use_tsqr) {
       a.RM1 = RM1;
       a.RM2 = RM2;
@@ -472,9 +477,14 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     }
     CK(cudaMemcpyAsync(c->h_status, c->d_status.p, (kStWords + 4) * sizeof(int),
                        cudaMemcpyDeviceToHost, c->st));
-    double acc[2];
-    CK(cudaMemcpyAsync(acc, c->d_acc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    double accs[2 * kAccSlots];
+    CK(cudaMemcpyAsync(accs, c->d_acc.p, sizeof(accs), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
+    double acc[2] = {0.0, 0.0};
+    for (int k = 0; k < kAccSlots; ++k) {
+      acc[0] += accs[2 * k];
+      acc[1] += accs[2 * k + 1];
+    }
     if (!c->h_status[kStOverflow]) {
       c->phase_flops[c->cur_phase] += acc[0];
       c->phase_bytes[c->cur_phase] += acc[1];
@@ -483,7 +493,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     const unsigned long long used =
         *reinterpret_cast<unsigned long long*>(c->h_status + kStWords);
     if (c->h_status[kStOverflow]) {
-      const size_t want = std::max<size_t>(out.arena.n + 1024, (size_t)(used * 1.1) + 1024);
+      const size_t want = std::max<size_t>(out.arena.n + 1024, (size_t)(used * 1.5) + 1024);
       out.arena.free();
       out.arena.alloc(want);
       continue;

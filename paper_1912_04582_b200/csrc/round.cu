@@ -827,8 +827,10 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
     p.out.ranks[2 * o] = t1;
     p.out.ranks[2 * o + 1] = t2;
     p.out.off[o] = ok ? (long long)at : -1;
-    atomicMax(&p.status[kStMaxR1], t1);
-    atomicMax(&p.status[kStMaxR2], t2);
+    // contended global atomics are spread / skipped: ranks only when larger,
+    // work counters over kAccSlots slots (summed by the host)
+    if (t1 > *(volatile int*)&p.status[kStMaxR1]) atomicMax(&p.status[kStMaxR1], t1);
+    if (t2 > *(volatile int*)&p.status[kStMaxR2]) atomicMax(&p.status[kStMaxR2], t2);
     if (p.acc) {
       double in_sz = 0.0;
       for (int k = 0; k < K; ++k)
@@ -837,8 +839,9 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
                  (terms[k].fb ? (double)n1 * terms[k].fa1 + (double)n2 * terms[k].fa1 * terms[k].fa2 +
                                     (double)terms[k].fa2 * n3
                               : 0.0);
-      atomicAdd(&p.acc[0], round_flops((double)n2, (double)R1, (double)R2, (double)t1, (double)t2));
-      atomicAdd(&p.acc[1], 8.0 * (in_sz + (double)sz));
+      double* slot = p.acc + 2 * (blockIdx.x % kAccSlots);
+      atomicAdd(&slot[0], round_flops((double)n2, (double)R1, (double)R2, (double)t1, (double)t2));
+      atomicAdd(&slot[1], 8.0 * (in_sz + (double)sz));
     }
     s_meta[2] = ok ? 1 : 0;
     reinterpret_cast<long long*>(sh)[20] = (long long)at;
@@ -1104,17 +1107,26 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
       else ei[q] = ej[q] = -1;
     }
   }
-  // X2_j = P blockdiag(M_j) (t1 x R2, ld t1), JB slices per phase
+  // X2_j = P blockdiag(M_j) (t1 x R2, ld t1), JB slices per phase.  When
+  // every slice's X2_j fits the region at once (small t1), they are kept for
+  // the output stage; when the W route staged all slices at once, cut 2
+  // reuses them.
   double* X2 = JB > 1 ? X2c : F;
+  const bool keepX2 =
+      (long long)n2 * t1 * R2 <= (long long)(JB > 1 ? JB * D1 * RMX : n1 * RMX);
+  const bool staged_all = wroute && JB >= n2;
   for (int j0 = 0; j0 < n2; j0 += JB) {
     const int jn = min(JB, n2 - j0);
+    double* X2j = keepX2 ? X2 + j0 * t1 * R2 : X2;
     __syncthreads();
-    stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
-    __syncthreads();
-    left_times_blockdiag_b(X2, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn);
+    if (!staged_all) {
+      stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
+      __syncthreads();
+    }
+    left_times_blockdiag_b(X2j, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn);
     __syncthreads();
     // S_j^T (q3 x t1) at column block jj
-    times_r3t_b(Tb, q3, q3 * t1, X2, t1, t1 * R2, t1, q3, R2, lastT, n3, jn);
+    times_r3t_b(Tb, q3, q3 * t1, X2j, t1, t1 * R2, t1, q3, R2, lastT, n3, jn);
     __syncthreads();
     gram_rows_acc<Q>(gh, gl, ei, ej, Tb, q3, jn * t1);
   }
@@ -1137,8 +1149,10 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
     p.out.ranks[2 * o] = t1;
     p.out.ranks[2 * o + 1] = t2;
     p.out.off[o] = ok ? (long long)at : -1;
-    atomicMax(&p.status[kStMaxR1], t1);
-    atomicMax(&p.status[kStMaxR2], t2);
+    // contended global atomics are spread / skipped: ranks only when larger,
+    // work counters over kAccSlots slots (summed by the host)
+    if (t1 > *(volatile int*)&p.status[kStMaxR1]) atomicMax(&p.status[kStMaxR1], t1);
+    if (t2 > *(volatile int*)&p.status[kStMaxR2]) atomicMax(&p.status[kStMaxR2], t2);
     if (p.acc) {
       double in_sz = 0.0;
       for (int k = 0; k < K; ++k)
@@ -1147,8 +1161,9 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
                  (terms[k].fb ? (double)n1 * terms[k].fa1 + (double)n2 * terms[k].fa1 * terms[k].fa2 +
                                     (double)terms[k].fa2 * n3
                               : 0.0);
-      atomicAdd(&p.acc[0], round_flops((double)n2, (double)R1, (double)R2, (double)t1, (double)t2));
-      atomicAdd(&p.acc[1], 8.0 * (in_sz + (double)sz));
+      double* slot = p.acc + 2 * (blockIdx.x % kAccSlots);
+      atomicAdd(&slot[0], round_flops((double)n2, (double)R1, (double)R2, (double)t1, (double)t2));
+      atomicAdd(&slot[1], 8.0 * (in_sz + (double)sz));
     }
     s_meta[2] = ok ? 1 : 0;
     reinterpret_cast<long long*>(sh)[20] = (long long)at;
@@ -1170,27 +1185,35 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
   });
   __syncthreads();
   const int kmax = min(n3, R2);
-  for (int s = threadIdx.x; s < t2; s += NT) {
-    double* g = Xs + mx * s;
-    for (int k = kmax - 1; k >= 0; --k) {
-      const double t = tau[k];
-      if (t == 0.0) continue;
-      double w = g[k];
-      for (int i = k + 1; i < n3; ++i) w += lastT[i + n3 * k] * g[i];
-      w *= t;
-      g[k] -= w;
-      for (int i = k + 1; i < n3; ++i) g[i] -= w * lastT[i + n3 * k];
+  {  // one warp per column of G, lanes over rows
+    const int lane = threadIdx.x & 31;
+    for (int s = threadIdx.x >> 5; s < t2; s += NW) {
+      double* g = Xs + mx * s;
+      for (int k = kmax - 1; k >= 0; --k) {
+        const double t = tau[k];
+        if (t == 0.0) continue;
+        const double* v = lastT + n3 * k;
+        double w = 0.0;
+        for (int i = k + 1 + lane; i < n3; i += 32) w += v[i] * g[i];
+        w = t * (warp_sum(w) + g[k]);
+        __syncwarp();
+        if (lane == 0) g[k] -= w;
+        for (int i = k + 1 + lane; i < n3; i += 32) g[i] -= w * v[i];
+        __syncwarp();
+      }
     }
   }
   __syncthreads();
   for2d(t2, n3, [&](int s, int kk) { dlast[s + t2 * kk] = Xs[kk + mx * s]; });
-  for (int j0 = 0; j0 < n2; j0 += JB) {
-    const int jn = min(JB, n2 - j0);
+  for (int j0 = 0; j0 < n2; j0 += (keepX2 ? n2 : JB)) {
+    const int jn = keepX2 ? n2 : min(JB, n2 - j0);
     __syncthreads();
-    stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
-    __syncthreads();
-    left_times_blockdiag_b(X2, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn);
-    __syncthreads();
+    if (!keepX2) {
+      stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
+      __syncthreads();
+      left_times_blockdiag_b(X2, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn);
+      __syncthreads();
+    }
     // middle_j = (P blockdiag(M_j)) Z
     for2d(t1, jn * t2, [&](int r, int js) {
       const int jj = js / t2, s = js - jj * t2;

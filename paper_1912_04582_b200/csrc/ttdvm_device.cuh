@@ -8,6 +8,7 @@ namespace ttdvm {
 
 constexpr int kMaxSets = 12;
 constexpr int kMaxTerms = 16;     // summands per rounded output
+constexpr int kAccSlots = 64;     // spread slots of the per-launch work counters
 constexpr int kRoundThreads = 128;
 // rank bins of a rounding launch: upper edges of max(R1, R2) of the summed input
 constexpr int kRankBins = 11;
@@ -84,7 +85,7 @@ struct RoundArgs {
   RoundOut out;
   int* status;                  // [kStWords]
   double* margins;              // optional [2*nout]
-  double* acc;                  // [2]: canonical FLOPs, compulsory bytes (atomicAdd)
+  double* acc;                  // [2 * kAccSlots]: canonical FLOPs, compulsory bytes
   unsigned long long* prof;     // optional [16] per-phase SM cycles (diagnostics)
   // shared-memory plan (doubles), chosen by the host launcher
   int RM1, RM2;                 // bounds on the summed input ranks
