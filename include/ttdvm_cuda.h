@@ -160,8 +160,8 @@ int ttdvm_cuda_face_factors(ttdvm_ctx* ctx, int32_t count, const double* normals
 int ttdvm_cuda_wall_densities(ttdvm_ctx* ctx, double* out);
 
 /* Set-up facts of the last step's mesh: [0] distinct oblique normals,
- * [1] of them with a kept singular value below 1e-12 sigma_max (FP64 Gram
- * noise level), [2] wall faces, [3] face-factor build time (microseconds). */
+ * [1] of them with a kept singular value below 1e-14 sigma_max (the FP64
+ * operand's own noise), [2] wall faces, [3] face-factor build time (us). */
 int ttdvm_cuda_setup_info(ttdvm_ctx* ctx, int64_t* info4);
 
 /* Device time (ms) of the kernels of the last call, by phase:

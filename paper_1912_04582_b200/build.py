@@ -50,5 +50,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+EXAMPLE_SRC = os.path.join(os.path.dirname(HERE), "examples", "shock_tube.cpp")
+EXAMPLE_BIN = os.path.join(os.path.dirname(HERE), "examples", "shock_tube")
+
+
+def build_example(force: bool = False) -> str:
+    """The C++ host driver (examples/shock_tube.cpp) over include/ttdvm_cuda.hpp,
+    linked against the in-tree library."""
+    lib = build()
+    if (not force and os.path.exists(EXAMPLE_BIN)
+            and os.path.getmtime(EXAMPLE_BIN) >= max(os.path.getmtime(EXAMPLE_SRC),
+                                                     os.path.getmtime(lib))):
+        return EXAMPLE_BIN
+    inc = os.path.join(os.path.dirname(HERE), "include")
+    subprocess.run([os.environ.get("CXX", "g++"), "-std=c++17", "-O2", "-I", inc, EXAMPLE_SRC,
+                    "-L", HERE, "-lttdvm_cuda", "-Wl,-rpath,$ORIGIN/../paper_1912_04582_b200",
+                    "-o", EXAMPLE_BIN], check=True)
+    return EXAMPLE_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

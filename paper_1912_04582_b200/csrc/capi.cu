@@ -235,7 +235,7 @@ struct ttdvm_ctx {
   TensorSet xin, eabs;
   std::vector<double> obl_normals;  // [3 * n_oblique]
   int n_oblique = 0;
-  int imprecise = 0;
+  int noise_floor = 0;
   double ff_ms = 0.0;
   // diffuse walls (T19): per wall face the xi_n^{+/-} factors, the unit
   // Maxwellian M(1, T_w, 0), the setup denominator and the per-step n_w
@@ -670,7 +670,7 @@ void build_oblique_factors(ttdvm_ctx* c) {
   if (c->h_status[kStError])
     throw Fail{TTDVM_EDOMAIN, "abs_xi_estimate: degenerate operand for oblique normal " +
                                   std::to_string(c->h_status[kStErrIdx])};
-  c->imprecise = c->h_status[kStAux];
+  c->noise_floor = c->h_status[kStAux];
   c->xin.used = sx * no;
   c->xin.maxr1 = c->xin.maxr2 = 2;
   c->eabs.used = se * no;
@@ -1438,7 +1438,7 @@ int ttdvm_cuda_face_factors(ttdvm_ctx* c, int32_t count, const double* normals, 
     if (c->h_status[kStError])
       throw Fail{TTDVM_EDOMAIN, "normal tensors: degenerate operand for normal " +
                                     std::to_string(c->h_status[kStErrIdx])};
-    c->imprecise = c->h_status[kStAux];
+    c->noise_floor = c->h_status[kStAux];
     c->result.used = st * count;
     c->result.maxr1 = c->result.maxr2 = cap;
     if (diag && count) CK(cudaMemcpy(diag, dd.p, 32LL * count, cudaMemcpyDeviceToHost));
@@ -1456,7 +1456,7 @@ int ttdvm_cuda_wall_densities(ttdvm_ctx* c, double* out) {
 int ttdvm_cuda_setup_info(ttdvm_ctx* c, int64_t* info4) {
   return guard(c, [&] {
     info4[0] = c->n_oblique;
-    info4[1] = c->imprecise;
+    info4[1] = c->noise_floor;
     info4[2] = c->nwall;
     info4[3] = (int64_t)(c->ff_ms * 1000.0);
   });

@@ -86,21 +86,24 @@ __device__ __forceinline__ void larfg(double alpha, double sigma2, double& beta,
 }
 
 // Visit (r, c) in [0, rows) x [0, cols) without integer division: threads
-// are split into power-of-two row lanes (r = tid & (rp - 1)) and column
-// strides.  No barriers or shuffles may be used inside f.
+// are split into power-of-two row lanes (r = tid & (rp - 1), rp <= NT) and
+// column strides; rows beyond rp wrap in an inner loop.  One code path per
+// lambda (instruction-cache footprint matters: the rounding kernel is
+// latency-bound and several CTAs per SM run different phases).  No
+// barriers or shuffles may be used inside f.
+constexpr int LOG_NT = NT == 32 ? 5 : (NT == 64 ? 6 : (NT == 128 ? 7 : 8));
 template <class Fn>
 __device__ __forceinline__ void for2d(int rows, int cols, Fn&& f) {
   if (rows <= 0 || cols <= 0) return;
-  const int lg = rows <= 1 ? 0 : 32 - __clz(rows - 1);
-  if ((1 << lg) <= NT) {
-    const int r = threadIdx.x & ((1 << lg) - 1);
-    if (r >= rows) return;
-    const int step = NT >> lg;
-    for (int c = threadIdx.x >> lg; c < cols; c += step) f(r, c);
-  } else {
-    for (int r = threadIdx.x; r < rows; r += NT)
-      for (int c = 0; c < cols; ++c) f(r, c);
-  }
+  int lg = rows <= 1 ? 0 : 32 - __clz(rows - 1);
+  lg = lg < LOG_NT ? lg : LOG_NT;
+  const int rp = 1 << lg;
+  const int r0 = threadIdx.x & (rp - 1);
+  if (r0 >= rows) return;
+  const int step = NT >> lg;
+  for (int c = threadIdx.x >> lg; c < cols; c += step)
+#pragma unroll 1
+    for (int r = r0; r < rows; r += rp) f(r, c);
 }
 
 __device__ __forceinline__ int floor_pow2(int x) {
@@ -120,6 +123,7 @@ __device__ int jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
   for (int sweep = 0; sweep < 60; ++sweep) {
     for (int j = threadIdx.x; j < c; j += NT) {
       double s = 0.0;
+#pragma unroll 1
       for (int i = 0; i < m; ++i) s += X[i + ldx * j] * X[i + ldx * j];
       nrm[j] = s;
     }
@@ -142,6 +146,7 @@ __device__ int jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
         double* x = X + ldx * (live ? a : 0);
         double* y = X + ldx * (live ? b : 0);
         if (live)
+#pragma unroll 1
           for (int i = sub; i < m; i += TPP) ga += x[i] * y[i];
         ga = group_sum<TPP>(ga);
         if (live && ga != 0.0) {
@@ -162,6 +167,7 @@ __device__ int jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
             const double t = (double)tf;
             rotated = rotated || (tf != 0.0f);  // an FP32-underflowed angle is converged
             const double cs = fast_rsqrt(1.0 + t * t), sn = cs * t;
+#pragma unroll 1
             for (int i = sub; i < m; i += TPP) {
               const double xi = x[i], yi = y[i];
               x[i] = cs * xi - sn * yi;

@@ -311,7 +311,7 @@ class Context:
     def setup_info(self) -> dict:
         info = np.zeros(4, dtype=np.int64)
         self._check(self.lib.ttdvm_cuda_setup_info(self.h, _ptr(info)))
-        return dict(oblique_normals=int(info[0]), imprecise_normals=int(info[1]),
+        return dict(oblique_normals=int(info[0]), noise_floor_normals=int(info[1]),
                     wall_faces=int(info[2]), face_factor_ms=float(info[3]) / 1000.0)
 
     def wall_densities(self) -> np.ndarray:
