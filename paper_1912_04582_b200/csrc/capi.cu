@@ -29,7 +29,9 @@ cudaError_t launch_round(const RoundArgs& a, cudaStream_t st);
 cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_round_bins(const RoundArgs& a, int* counts, int* bmax, int* lists,
                               cudaStream_t st);
-size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX, int JB);
+size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX, int JB, bool spill);
+long long round_gram_spill_doubles(int n1, int n3, int RM1, int RM2);
+cudaError_t round_gram_resident(const RoundArgs& a, int* resident);
 size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int MSMAX);
 struct MacroArgs {
   TSet set;
@@ -248,6 +250,7 @@ struct ttdvm_ctx {
   int* h_status = nullptr;  // pinned, kStWords + 2 longs
   DevBuf<double> d_margins;
   DevBuf<int> d_bins, d_olist;  // rank bins of the current rounding launch
+  DevBuf<double> d_gscratch;     // per-CTA slices of spill-plan rounding launches
   DevBuf<long long> d_tmp_off;
   DevBuf<double> d_tmp;
   bool profiling = false;
@@ -396,47 +399,54 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     MSMAX = std::max(MSMAX, bmax[4 * b + 2]);
   }
   const int mx = n;
-  if (mx > 48) throw Fail{TTDVM_EINVAL, "velocity grids above 48 nodes per axis are not supported"};
   // exact-Gram route by default; TTDVM_ROUND=tsqr selects the Householder
-  // TSQR route (kept for A/B comparison; one launch, global bounds)
+  // TSQR route (kept for A/B comparison; one launch, global bounds, n <= 48)
   static const bool use_tsqr = [] {
     const char* e = getenv("TTDVM_ROUND");
     return e && std::string(e) == "tsqr";
   }();
   int HMAX = mx;
   if (use_tsqr) {
+    if (mx > 48) throw Fail{TTDVM_EINVAL, "the TSQR route supports at most 48 nodes per axis"};
     HMAX = mx <= 32 ? mx : 48;
     if (round_smem_bytes(n, n, n, RM1, RM2, HMAX, MSMAX) > 227 * 1024)
       throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory"};
   }
+  constexpr size_t kSmemMax = 227 * 1024;
   struct Launch {
     int bin, count, rm1, rm2, ms, jb;
+    bool spill;
   };
   // slices per barrier phase: about a quarter of the slices (measured best
   // on config 4: fewer phases pay for a lower CTA count), shrunk while the
   // plan would leave fewer than 3 CTAs per SM
   auto pick_jb = [&](int rm1, int rm2, int ms) {
-    const size_t base = round_gram_smem_bytes(n, n, rm1, rm2, ms, 1);
+    const size_t base = round_gram_smem_bytes(n, n, rm1, rm2, ms, 1, false);
     const size_t budget = std::max(base, (size_t)(228 * 1024 / 3) - 2048);
     int jb = (n + 3) / 4;
-    while (jb > 1 && round_gram_smem_bytes(n, n, rm1, rm2, ms, jb) > budget) --jb;
+    while (jb > 1 && round_gram_smem_bytes(n, n, rm1, rm2, ms, jb, false) > budget) --jb;
     return jb;
   };
   std::vector<Launch> plan;
   for (int b = kRankBins - 1; b >= 0; --b) {  // large ranks first (long CTAs start early)
     if (!bcount[b]) continue;
     Launch l{b, bcount[b], std::max(1, bmax[4 * b]), std::max(1, bmax[4 * b + 1]),
-             std::max(1, bmax[4 * b + 2]), 1};
-    l.jb = use_tsqr ? 1 : pick_jb(l.rm1, l.rm2, l.ms);
+             std::max(1, bmax[4 * b + 2]), 1, false};
+    // working sets above the shared-memory budget (n = 64, summed ranks of
+    // ~100 and more) take the spill plan: F, last^T, XP and the Gram region
+    // in a per-CTA global scratch slice, persistent CTAs
+    l.spill = !use_tsqr && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false) > kSmemMax;
+    l.jb = (use_tsqr || l.spill) ? 1 : pick_jb(l.rm1, l.rm2, l.ms);
     static const int force_jb = [] {  // diagnostics: TTDVM_JB=k forces k slices per phase
       const char* e = getenv("TTDVM_JB");
       return e ? atoi(e) : 0;
     }();
-    if (force_jb > 0 && !use_tsqr) {
+    if (force_jb > 0 && !use_tsqr && !l.spill) {
       l.jb = std::min(n, force_jb);
-      while (l.jb > 1 && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, l.jb) > 227 * 1024) --l.jb;
+      while (l.jb > 1 && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, l.jb, false) > kSmemMax)
+        --l.jb;
     }
-    if (!use_tsqr && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1) > 227 * 1024)
+    if (l.spill && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, true) > kSmemMax)
       throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory (n=" +
                                    std::to_string(n) + ", summed ranks " +
                                    std::to_string(l.rm1) + "x" + std::to_string(l.rm2) + ")"};
@@ -471,7 +481,20 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
         a.MSMAX = l.ms;
         a.JB = l.jb;
         a.olist = c->d_olist.p + (size_t)l.bin * nout;
-        CK(launch_round_gram(a, l.count, c->st));
+        a.gscratch = nullptr;
+        a.gstride = 0;
+        a.nblk = l.count;
+        int grid = l.count;
+        if (l.spill) {
+          int resident = 0;
+          CK(round_gram_resident(a, &resident));
+          if (resident <= 0) throw Fail{TTDVM_ENOMEM, "spill rounding plan does not fit an SM"};
+          grid = std::min(l.count, resident);
+          a.gstride = round_gram_spill_doubles(n, n, l.rm1, l.rm2);
+          c->d_gscratch.alloc((size_t)grid * (size_t)a.gstride);
+          a.gscratch = c->d_gscratch.p;
+        }
+        CK(launch_round_gram(a, grid, c->st));
         c->launches += 1;
       }
     }

@@ -917,48 +917,83 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
 // as the Householder R (rounding R to FP64) -- the rank decisions keep the
 // accuracy of the QR route -- while the slice loop has no sequential
 // column steps (3 barriers per slice instead of 2 per column).
-template <int Q>
-__global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_kernel(RoundArgs p) {
-  extern __shared__ double sm[];
+// Buffer plan of the exact-Gram kernel (doubles).  Shared: everything;
+// with `spill`, F, last^T, XP and the Gram region move to a per-CTA global
+// scratch slice (gdoubles) and JB must be 1.
+struct GramPlan {
+  int mx, RMX, D1, D3, D, GZ, TBZ;
+};
+__host__ __device__ inline GramPlan gram_plan(int n1, int n3, int RM1, int RM2, int JB) {
+  GramPlan g;
+  g.mx = n1 > n3 ? n1 : n3;
+  g.RMX = RM1 > RM2 ? RM1 : RM2;
+  g.D1 = n1 < RM1 ? n1 : RM1;
+  g.D3 = n3 < RM2 ? n3 : RM2;
+  g.D = g.D1 > g.D3 ? g.D1 : g.D3;
+  g.GZ = 2 * g.D * g.D > RM2 * g.D ? 2 * g.D * g.D : RM2 * g.D;
+  g.TBZ = g.mx * g.D > JB * g.D1 * g.D3 ? g.mx * g.D : JB * g.D1 * g.D3;
+  return g;
+}
+
+// One output per call (one CTA of NT threads).  SPILL: see gram_plan.
+template <int Q, bool SPILL>
+__device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o, double* sm,
+                                                int* s_meta) {
   const int n1 = p.n1, n2 = p.n2, n3 = p.n3;
-  const int mx = max(n1, n3);
   const int RM1 = p.RM1, RM2 = p.RM2;
-  const int RMX = max(RM1, RM2);
   // Buffers scale with D = max(min(n1, RM1), min(n3, RM2)) -- the largest
   // Gram / SVD dimension of this launch -- not with n^2, so launches of
   // low-rank sums (the rank bins of run_round) fit several CTAs per SM.
-  const int D1 = min(n1, RM1), D3 = min(n3, RM2), D = max(D1, D3);
-  const int GZ = max(2 * D * D, RM2 * D);
   // JB slices per barrier phase in the W route, cut 2 and the output (the
   // T route stages one slice at a time); chosen by the host from the budget
-  const int JB = p.JB;
-  const int TBZ = max(mx * D, JB * D1 * D3);
-  double* F = sm;                          // n1 x RMX   (cut 2 / output: X2 when JB = 1)
-  double* lastT = F + n1 * RMX;            // n3 x RM2
-  double* tau = lastT + n3 * RM2;          // mx
-  double* Tb = tau + mx;                   // TBZ        (slice blocks, C^T; V2 at the end)
-  double* G = Tb + TBZ;                    // GZ         (Gram hi/lo planes; Z at the end)
+  const int JB = SPILL ? 1 : p.JB;
+  const GramPlan gp = gram_plan(n1, n3, RM1, RM2, JB);
+  const int mx = gp.mx, RMX = gp.RMX, D1 = gp.D1, D3 = gp.D3, D = gp.D;
+  double* cur = sm;
+  double *F, *lastT, *XP, *G;
+  if (SPILL) {
+    F = p.gscratch + (long long)blockIdx.x * p.gstride;  // n1 x RMX
+    lastT = F + n1 * RMX;                                 // n3 x RM2
+    XP = lastT + n3 * RM2;                                // n1 x RMX
+    G = XP + n1 * RMX;                                    // GZ
+  } else {
+    F = cur;                       // n1 x RMX   (cut 2 / output: X2 when JB = 1)
+    cur += n1 * RMX;
+    lastT = cur;                   // n3 x RM2
+    cur += n3 * RM2;
+  }
+  double* tau = cur;               // mx
+  cur += mx;
+  double* Tb = cur;                // TBZ        (slice blocks, C^T; V2 at the end)
+  cur += gp.TBZ;
+  if (!SPILL) {
+    G = cur;                       // GZ         (Gram hi/lo planes; Z at the end)
+    cur += gp.GZ;
+    XP = cur;                      // n1 x RMX   (cut 1: X; cut 2: P)
+    cur += n1 * RMX;
+  }
   double* Gl = G + D * D;
-  double* XP = G + GZ;                     // n1 x RMX   (cut 1: X; cut 2: P)
-  double* U1 = XP + n1 * RMX;              // n1 x D1
-  double* Xs = U1 + n1 * D1;               // mx x D     (Jacobi workspace)
-  double* Rc = Xs + mx * D;                // D x D      (Cholesky factor)
-  double* Ms = Rc + D * D;                 // JB x p.MSMAX (staged middle slices)
-  double* X2c = Ms + JB * p.MSMAX;         // JB x D1 x RMX when JB > 1 (P M_j per slice)
-  double* sig = X2c + (JB > 1 ? JB * D1 * RMX : 0);  // mx
-  double* sraw = sig + mx;                 // mx
-  double* vn = sraw + mx;                  // mx
-  double* sh = vn + mx;                    // 32 scalars
+  double* U1 = cur;                // n1 x D1
+  cur += n1 * D1;
+  double* Xs = cur;                // mx x D     (Jacobi workspace)
+  cur += mx * D;
+  double* Rc = cur;                // D x D      (Cholesky factor)
+  cur += D * D;
+  double* Ms = cur;                // JB x p.MSMAX (staged middle slices)
+  cur += JB * p.MSMAX;
+  double* X2c = cur;               // JB x D1 x RMX when JB > 1 (P M_j per slice)
+  cur += JB > 1 ? JB * D1 * RMX : 0;
+  double* sig = cur;               // mx
+  double* sraw = sig + mx;         // mx
+  double* vn = sraw + mx;          // mx
+  double* sh = vn + mx;            // 32 scalars
   int* perm = reinterpret_cast<int*>(sh + 32);          // mx
   int* piv = perm + mx;                                  // mx
   int* colterm = piv + mx;                               // RM2
   int* rowterm = colterm + RM2;                          // RM1
   TermInfo* terms = reinterpret_cast<TermInfo*>(
       reinterpret_cast<double*>(rowterm + RM1 + (((RM1 + RM2) & 1) ? 1 : 0)));
-  __shared__ int s_meta[8];
 
-  const int o = p.olist ? p.olist[blockIdx.x] : blockIdx.x;
-  if (o >= p.nout) return;
   long long prof_t = p.prof ? clock64() : 0;
 #define PROF(k)                                                      \
   if (p.prof && threadIdx.x == 0) {                                  \
@@ -1234,32 +1269,67 @@ __global__ void __launch_bounds__(NT, Q == 1 ? 6 : (Q == 3 ? 4 : 3)) round_gram_
 #undef PROF
 }
 
-size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX, int JB) {
-  const size_t mx = n1 > n3 ? n1 : n3;
-  const size_t RMX = RM1 > RM2 ? RM1 : RM2;
-  const size_t D1 = n1 < RM1 ? n1 : RM1, D3 = n3 < RM2 ? n3 : RM2;
-  const size_t D = D1 > D3 ? D1 : D3;
-  const size_t GZ = 2 * D * D > (size_t)RM2 * D ? 2 * D * D : (size_t)RM2 * D;
-  const size_t TBZ = mx * D > JB * D1 * D3 ? mx * D : JB * D1 * D3;
-  size_t d = (size_t)n1 * RMX + (size_t)n3 * RM2 + mx + TBZ + GZ + (size_t)n1 * RMX +
-             (size_t)n1 * D1 + mx * D + D * D + (size_t)JB * MSMAX +
-             (JB > 1 ? (size_t)JB * D1 * RMX : 0) + 3 * mx + 32;
-  size_t ints = 2 * mx + RM2 + RM1 + 1;
+// Shared-memory plans: one CTA per output (6 / 4 / 3 CTAs per SM by Gram
+// size); SPILL launches are persistent (grid = resident CTAs) and loop.
+template <int Q, bool SPILL>
+__global__ void __launch_bounds__(NT, SPILL ? 1 : (Q == 1 ? 6 : (Q == 3 ? 4 : (Q <= 10 ? 3 : 1))))
+    round_gram_kernel(RoundArgs p) {
+  extern __shared__ double sm[];
+  __shared__ int s_meta[8];
+  if (!SPILL) {
+    const int o = p.olist ? p.olist[blockIdx.x] : blockIdx.x;
+    if (o < p.nout) round_gram_body<Q, false>(p, o, sm, s_meta);
+    return;
+  }
+  for (int b = blockIdx.x; b < p.nblk; b += gridDim.x) {
+    const int o = p.olist ? p.olist[b] : b;
+    __syncthreads();  // the previous output's shared-memory readers are done
+    if (o < p.nout) round_gram_body<Q, true>(p, o, sm, s_meta);
+  }
+}
+
+size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX, int JB, bool spill) {
+  if (spill) JB = 1;
+  const GramPlan g = gram_plan(n1, n3, RM1, RM2, JB);
+  const size_t big = spill ? 0
+                           : (size_t)n1 * g.RMX + (size_t)n3 * RM2 + (size_t)g.GZ +
+                                 (size_t)n1 * g.RMX;
+  size_t d = big + g.mx + g.TBZ + (size_t)n1 * g.D1 + (size_t)g.mx * g.D + (size_t)g.D * g.D +
+             (size_t)JB * MSMAX + (JB > 1 ? (size_t)JB * g.D1 * g.RMX : 0) + 3 * g.mx + 32;
+  size_t ints = 2 * g.mx + RM2 + RM1 + 1;
   return d * 8 + ((ints * 4 + 7) / 8) * 8 + sizeof(TermInfo) * kMaxTerms + 64;
 }
 
-cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st) {
-  if (nblocks == 0) return cudaSuccess;
-  const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX, a.JB);
+// Doubles of one CTA's global scratch slice in the spill plan (32-aligned).
+long long round_gram_spill_doubles(int n1, int n3, int RM1, int RM2) {
+  const GramPlan g = gram_plan(n1, n3, RM1, RM2, 1);
+  const long long d = 2LL * n1 * g.RMX + (long long)n3 * RM2 + g.GZ;
+  return (d + 31) / 32 * 32;
+}
+
+template <bool SPILL>
+static cudaError_t launch_gram_q(const RoundArgs& a, int grid, size_t smem, cudaStream_t st,
+                                 int* resident) {
   const int D1 = a.n1 < a.RM1 ? a.n1 : a.RM1, D3 = a.n3 < a.RM2 ? a.n3 : a.RM2;
   const int D = D1 > D3 ? D1 : D3;
   const int ne = D * (D + 1) / 2;
   cudaError_t e = cudaSuccess;
-#define LAUNCH_Q(QV)                                                                          \
-  e = cudaFuncSetAttribute(round_gram_kernel<QV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)smem);                                                         \
-  if (e != cudaSuccess) return e;                                                              \
-  round_gram_kernel<QV><<<nblocks, NT, smem, st>>>(a);
+#define LAUNCH_Q(QV)                                                                         \
+  {                                                                                          \
+    auto kern = round_gram_kernel<QV, SPILL>;                                                \
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+    if (e != cudaSuccess) return e;                                                          \
+    if (resident) {                                                                          \
+      int per = 0, dev = 0, sms = 0;                                                         \
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, smem);               \
+      if (e != cudaSuccess) return e;                                                        \
+      cudaGetDevice(&dev);                                                                   \
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                     \
+      *resident = per * sms;                                                                 \
+      return cudaSuccess;                                                                    \
+    }                                                                                        \
+    kern<<<grid, NT, smem, st>>>(a);                                                         \
+  }
   if (ne <= NT) {
     LAUNCH_Q(1)
   } else if (ne <= 3 * NT) {
@@ -1268,11 +1338,30 @@ cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st) 
     LAUNCH_Q(5)
   } else if (ne <= 10 * NT) {
     LAUNCH_Q(10)
+  } else if (ne <= 17 * NT) {
+    LAUNCH_Q(17)
   } else {
     return cudaErrorInvalidValue;
   }
 #undef LAUNCH_Q
   return cudaGetLastError();
+}
+
+// Resident CTAs of the spill plan (persistent grid size), from the occupancy API.
+cudaError_t round_gram_resident(const RoundArgs& a, int* resident) {
+  const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX, 1, true);
+  return launch_gram_q<true>(a, 0, smem, nullptr, resident);
+}
+
+// a.gscratch != null selects the spill plan: grid CTAs loop over a.nblk outputs.
+cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st) {
+  if (nblocks == 0) return cudaSuccess;
+  if (a.gscratch) {
+    const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX, 1, true);
+    return launch_gram_q<true>(a, nblocks, smem, st, nullptr);
+  }
+  const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX, a.JB, false);
+  return launch_gram_q<false>(a, nblocks, smem, st, nullptr);
 }
 
 // Shared-memory bytes of the plan above.

@@ -92,6 +92,12 @@ struct RoundArgs {
   int HMAX;                     // rows of the TSQR block buffer
   int MSMAX;                    // doubles of the staged middle slices
   int JB;                       // slices per barrier phase (exact-Gram kernel)
+  // spill plan (working sets above the shared-memory budget: n = 64, large
+  // summed ranks): the four largest buffers live in a per-CTA global scratch
+  // slice (L1/L2-resident) and the launch is persistent over nblk outputs
+  double* gscratch;             // [gridDim.x * gstride] or null
+  long long gstride;            // doubles per CTA slice
+  int nblk;                     // outputs of this launch (persistent loop bound)
 };
 
 }  // namespace ttdvm

@@ -164,6 +164,25 @@ def obstacle_flow(shape=(100, 80, 64), hole: int = 8, nv: int = 44, bound: float
                                                                  hole=hole, seed=seed))
 
 
+def rounding_summands(rng: np.random.Generator, count: int, n: int = 32, terms: int = 6,
+                      rank: int = 12, decay: float = 0.5):
+    """Config 3 inputs: ``count`` independent sums of ``terms`` seeded TT
+    tensors of ranks (1, rank, rank, 1) on n^3.  Core entries are N(0,1);
+    the "geometric singular-value decay of 0.5 per index" is put on the
+    rank indices of the outer cores: column a of the first core is scaled by
+    decay^a and row b of the last core by decay^b (the middle core stays
+    N(0,1)).  DESIGN.md records this reading.  Returns (first, middle, last)
+    arrays of shapes (count*terms, n, rank), (count*terms, n, rank, rank),
+    (count*terms, rank, n) in the reference's index order (first[t, i, a],
+    middle[t, j, a, b], last[t, b, k])."""
+    m = count * terms
+    w = decay ** np.arange(rank)
+    first = rng.standard_normal((m, n, rank)) * w[None, None, :]
+    middle = rng.standard_normal((m, n, rank, rank))
+    last = rng.standard_normal((m, rank, n)) * w[None, :, None]
+    return first, middle, last
+
+
 def config(idx: int, scale: float = 1.0) -> Problem:
     """BASELINE.json configs by 1-based index; ``scale`` < 1 shrinks the
     spatial mesh for parity tests (velocity mesh unchanged)."""

@@ -108,6 +108,49 @@ def test_round_t_route_and_cap(ctx):
     assert got.ranks.max() <= 3
 
 
+def decaying_tt(rng, n, r, decay=0.5):
+    """N(0,1) cores with decay^a on the outer cores' rank indices (config 3 style)."""
+    w = decay ** np.arange(r)
+    return TtTensor(rng.standard_normal((n, r)) * w[None, :], rng.standard_normal((n, r, r)),
+                    rng.standard_normal((r, n)) * w[:, None])
+
+
+def test_round_spill_plan_n64_t_route_cap(ctx):
+    """n = 64 with summed ranks 140 (config 5's cell residual at cap 20: six
+    face fluxes + J): the working set exceeds shared memory, so the launch
+    takes the spill plan (global scratch slices, persistent CTAs), T route."""
+    rng = np.random.default_rng(64)
+    n = 64
+    groups = [[(random_tt(rng, n, n, n, 20, 20), float(rng.standard_normal())) for _ in range(7)]
+              for _ in range(3)]
+    got, _ = check_round(ctx, groups, 1e-5, cap=20)
+    assert got.ranks.max() == 20
+
+
+def test_round_spill_plan_n64_w_route(ctx):
+    """n = 64, summed ranks 60 < n (W route) with decaying spectra, no cap:
+    spill plan, rank decisions against the oracle's margins."""
+    rng = np.random.default_rng(65)
+    n = 64
+    groups = [[(decaying_tt(rng, n, 20, 0.3), 1.0), (decaying_tt(rng, n, 20, 0.3), -0.7),
+               (decaying_tt(rng, n, 20, 0.3), 0.4)] for _ in range(3)]
+    _, flips = check_round(ctx, groups, 1e-6)
+    assert flips <= 1
+
+
+def test_round_config3_shape(ctx):
+    """Config 3 inputs (32^3, six rank-12 summands with 0.5 decay, rank 72
+    summed) at a few tensors: every reading gives full ranks (32, 32)."""
+    from paper_1912_04582_b200.problems import rounding_summands
+    rng = np.random.default_rng(3)
+    f, m, l = rounding_summands(rng, 3)
+    groups = [[(TtTensor(f[6 * g + k], m[6 * g + k], l[6 * g + k]), 1.0) for k in range(6)]
+              for g in range(3)]
+    got, flips = check_round(ctx, groups, 1e-6)
+    assert flips == 0
+    assert all(tuple(r) == (32, 32) for r in got.ranks)
+
+
 def test_round_reference_edge_cases(ctx):
     rng = np.random.default_rng(31)
     a = random_tt(rng, 8, 8, 8, 2, 3)
@@ -233,6 +276,15 @@ def test_step_config1_shock_tube(ctx):
 
 def test_step_config2_small(ctx):
     p = config(2, scale=3 / 32)
+    worst, flips = check_step(ctx, p, 2)
+    assert flips <= 1
+
+
+def test_step_config5_small(ctx):
+    """Config 5's velocity mesh (64^3 on [-8,8]^3, eps 1e-5, cap 20) on a
+    2x2x2 periodic box: n = 64 through the whole step."""
+    p = config(5, scale=2 / 128)
+    assert p.nv == 64 and p.cap == 20
     worst, flips = check_step(ctx, p, 2)
     assert flips <= 1
 
