@@ -11,7 +11,11 @@ one-time face-factor set-up (|xi_n| estimates of 1.5 M distinct oblique
 normals) is timed separately (config.setup_s), not inside the step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 1|2|4|5] [--scale s]
+                    [--config 1|2|3|4|5] [--scale s]
+
+--config 3 is the batched-rounding microbench (rounded tensors/s; a step
+rounds one resident chunk of 8192 x scale config-3 sums, the 2^20 tensors
+of the config being 128 such chunks of identical per-tensor work).
 
 N > 1 under torchrun: config 4 is partitioned by recursive coordinate
 bisection of the cell centroids (strong scaling, the same mesh on N GPUs);
@@ -121,9 +125,20 @@ def traffic_from_profiles():
 
 
 # ------------------------------------------------------------------ CPU arms
-def _ref_worker_init(args_tuple):
+def _one_blas_thread():
+    """numpy is imported with this module (also in spawned workers), so the
+    BLAS pool is limited at run time, not through the environment."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     os.environ["OMP_NUM_THREADS"] = "1"
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+
+
+def _ref_worker_init(args_tuple):
+    _one_blas_thread()
     global _W
     cfg, scale = args_tuple
     from oracle.step import OracleSolver
@@ -204,11 +219,181 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------- config 3: batched rounding
+C3_CHUNK = 8192
+
+
+def c3_inputs(count: int, seed: int = 3):
+    from paper_1912_04582_b200.problems import rounding_summands
+    from paper_1912_04582_b200.tt_batch import TtBatch
+    f, m, l = rounding_summands(np.random.default_rng(seed), count)
+    b = TtBatch.uniform(6 * count, 32, 32, 32, 12, 12, f, m, l)
+    return b, np.arange(0, 6 * count + 1, 6, dtype=np.int64)
+
+
+def _c3_task(args_tuple):
+    _one_blas_thread()
+    from oracle.tt import TtTensor
+    from paper_1912_04582_b200.problems import rounding_summands
+    seed, count = args_tuple
+    f, m, l = rounding_summands(np.random.default_rng(seed), count)
+    sums = []
+    for g in range(count):
+        s = TtTensor(f[6 * g], m[6 * g], l[6 * g])
+        for k in range(1, 6):
+            s = s + TtTensor(f[6 * g + k], m[6 * g + k], l[6 * g + k])
+        sums.append(s)
+    t = time.perf_counter()
+    for s in sums:
+        s.rounded(1e-6)
+    return time.perf_counter() - t
+
+
+def c3_cpu_rate(workers: int, per: int, repeats: int = 1):
+    import multiprocessing as mp
+    ctxm = mp.get_context("spawn")
+    with ctxm.Pool(workers) as pool:
+        best = None
+        for r in range(repeats):
+            t = time.perf_counter()
+            pool.map(_c3_task, [(100 + w, per) for w in range(workers)])
+            el = time.perf_counter() - t
+            best = el if best is None else min(best, el)
+    return workers * per / best
+
+
+def c3_config(count):
+    return {"workload": "config3-batched-rounding", "config_index": 3,
+            "tensors_per_step": count, "tensor_shape": "32x32x32",
+            "summands": "6 x rank-(1,12,12,1), N(0,1) cores, 0.5^a decay on the outer cores' "
+                        "rank indices (summed rank 72)", "eps": 1e-6,
+            "full_config": "2^20 tensors = %d chunks of identical per-tensor work" % (
+                (1 << 20) // count),
+            "l2_policy": "inputs larger than L2 (%.1f GB resident summands)" % (
+                count * 6 * (32 * 12 * 2 + 32 * 144) * 8 / 1e9)}
+
+
+def run_config3(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    count = max(16, int(C3_CHUNK * args.scale))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        workers = os.cpu_count() or 1
+        per = 32
+        c3_cpu_rate(workers, 1)  # warm the pool imports
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            c3_cpu_rate(workers, per)
+        value = workers * per * args.steps / (time.perf_counter() - t)
+        print(json.dumps({"impl": "reference", "metric": "rounded tensors/s", "value": value,
+                          "unit": "tensors/s", "n_gpus": args.gpus, "steps": args.steps,
+                          "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "config": c3_config(count),
+                          "cpu_baseline": {"value": value, "unit": "tensors/s", "cores": workers,
+                                           "kind": "port",
+                                           "sample": f"{workers} processes x {per} config-3 sums "
+                                                     "per step, numpy oracle rounded(1e-6)"},
+                          "e2e": {"value": value, "unit": "tensors/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1912_04582_b200.cuda import Context
+    b, go = c3_inputs(count, seed=3 + rank)  # independent tensors per rank: weak scaling
+    ctx = Context(local)
+    ctx.set_grid(32, 1.0)
+    eps = 1e-6
+    ctx.rounded(b, eps, 0, group_off=go)  # upload; the inputs stay resident
+    ctx.round_resident(eps, 0, args.warmup)
+    ctx.set_profiling(True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = ctx.round_resident(eps, 0, args.steps)
+    torch.cuda.synchronize()
+    flops, bytes_, launches = ctx.phase_work()
+    phase_ms = ctx.phase_times()
+    gpu_launches = ctx.launch_count()
+    res = ctx.result()
+    ranks = res.ranks
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * count * args.steps / (ms / 1e3)
+    ctx.set_profiling(False)
+    # e2e: host summands -> device, round, result -> host, every step
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(args.e2e_steps):
+        out = ctx.rounded(b, eps, 0, group_off=go)
+        d2h += int(out.cores.nbytes + out.ranks.nbytes + out.offsets.nbytes)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = int(b.cores.nbytes + b.ranks.nbytes + b.offsets.nbytes + go.nbytes)
+    fp64_peak = ctx.fp64_peak()
+    dom_s = phase_ms[2] / 1e3
+    achieved = flops[2] / dom_s / 1e12 if dom_s > 0 else 0.0
+    traffic = traffic_from_profiles().get("config3")
+    roofline = {"bound": "fp64", "kernel": "round_gram_kernel (config-3 T route)",
+                "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak if fp64_peak else None,
+                "peak_source": "measured on this GPU by the DFMA probe in libttdvm_cuda.so",
+                "flops_per_launch": flops[2] / max(1, launches[2]),
+                "flops_per_tensor": flops[2] / (count * args.steps),
+                "launch_ms": phase_ms[2] / max(1, launches[2]),
+                "algorithmic_bytes_per_launch": bytes_[2] / max(1, launches[2]),
+                "hbm_frac": (bytes_[2] / dom_s / 1e9) / load_peaks().get("hbm_gbs", 6547.8)
+                if dom_s > 0 else None,
+                "traffic": traffic}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        per = 1024
+        rate = c3_cpu_rate(1, per)
+        cpu = {"value": rate, "unit": "tensors/s", "cores": 1, "kind": "port",
+               "sample": f"{per} config-3 sums rounded at 1e-6 by the numpy oracle "
+                         "(oracle/tt.py), 1 process, 1 BLAS thread"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "rounded tensors/s", "value": value, "unit": "tensors/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": dict(c3_config(count), parallelism=f"independent chunks x{world}"
+                           if world > 1 else "single GPU",
+                           output_ranks={"min": ranks.min(0).tolist(),
+                                         "max": ranks.max(0).tolist()}),
+            "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": world * count * args.e2e_steps / e2e_s, "unit": "tensors/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h // args.e2e_steps,
+                    "steps": args.e2e_steps},
+            "gpu_launches": gpu_launches, "clocks": clk.summary()}), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
     if args.e2e_steps <= 0:
         args.e2e_steps = args.steps
+    if args.config == 3:
+        run_config3(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return

@@ -131,6 +131,12 @@ int ttdvm_cuda_stage_download(ttdvm_ctx* ctx, int32_t set, double* cores, int64_
 int ttdvm_cuda_round_batch(ttdvm_ctx* ctx, const ttdvm_tt_batch* in, int32_t nout,
                            const int64_t* group_off, const double* scale, double eps,
                            int32_t cap, double* margins);
+/* Re-round the input batch and sums of the last ttdvm_cuda_round_batch call,
+ * already resident on the device (config-3 microbench: inputs in HBM),
+ * `repeats` times; *ms = device time of all repeats (CUDA events on the
+ * library stream).  Same kernels and result as ttdvm_cuda_round_batch. */
+int ttdvm_cuda_round_resident(ttdvm_ctx* ctx, double eps, int32_t cap, int32_t repeats,
+                              double* ms);
 int ttdvm_cuda_result_layout(ttdvm_ctx* ctx, int32_t* ranks, int64_t* offsets);
 int ttdvm_cuda_result_download(ttdvm_ctx* ctx, double* cores, int64_t capacity);
 

@@ -1362,6 +1362,34 @@ int ttdvm_cuda_round_batch(ttdvm_ctx* c, const ttdvm_tt_batch* in, int32_t nout,
   });
 }
 
+int ttdvm_cuda_round_resident(ttdvm_ctx* c, double eps, int32_t cap, int32_t repeats,
+                              double* ms) {
+  return guard(c, [&] {
+    require(eps > 0.0, "rounded: eps must be > 0");
+    require(c->t_batch.nout() > 0, "ttdvm_cuda_round_batch first");
+    require(repeats >= 1, "repeats must be >= 1");
+    cudaSetDevice(c->device);
+    TensorSet* sets[kMaxSets] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &c->in};
+    reset_counters(c);
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaEventRecord(a, c->st));
+    for (int k = 0; k < repeats; ++k) {
+      Timer t(c, 2);
+      run_round(c, c->t_batch, sets, c->result, eps, cap, nullptr);
+    }
+    CK(cudaEventRecord(b, c->st));
+    CK(cudaEventSynchronize(b));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (ms) *ms = f;
+  });
+}
+
 int ttdvm_cuda_result_layout(ttdvm_ctx* c, int32_t* ranks, int64_t* offsets) {
   return guard(c, [&] { layout_of(c, c->result, ranks, offsets); });
 }

@@ -34,6 +34,7 @@ EXPORTS = (
     "ttdvm_cuda_timed_step", "ttdvm_cuda_fp64_peak", "ttdvm_cuda_round_profile",
     "ttdvm_cuda_set_owned", "ttdvm_cuda_halo_pack", "ttdvm_cuda_halo_unpack",
     "ttdvm_cuda_face_factors", "ttdvm_cuda_wall_densities", "ttdvm_cuda_setup_info",
+    "ttdvm_cuda_round_resident",
 )
 
 OK, EINVAL, EDOMAIN, ENOMEM, ECUDA, ENCCL = range(6)
@@ -97,6 +98,7 @@ def load_library(path: str = LIB_PATH):
         "ttdvm_cuda_face_factors": (C.c_int, [vp, i32, vp, i32, i32, vp]),
         "ttdvm_cuda_wall_densities": (C.c_int, [vp, vp]),
         "ttdvm_cuda_setup_info": (C.c_int, [vp, vp]),
+        "ttdvm_cuda_round_resident": (C.c_int, [vp, dbl, i32, i32, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -269,11 +271,25 @@ class Context:
         mg = np.zeros(2 * max(nout, 1)) if margins else None
         self._check(self.lib.ttdvm_cuda_round_batch(self.h, C.byref(s), nout, _ptr(go), _ptr(sc),
                                                     float(eps), int(cap), _ptr(mg)))
+        self._last_nout = nout
         out = self._fetch(nout, lambda r, o: self.lib.ttdvm_cuda_result_layout(self.h, r, o),
                           lambda c, cap_: self.lib.ttdvm_cuda_result_download(self.h, c, cap_))
         if margins:
             return out, mg[:2 * nout].reshape(nout, 2)
         return out
+
+    def round_resident(self, eps: float, cap: int = 0, repeats: int = 1) -> float:
+        """Repeat the last rounded() on its device-resident inputs; device ms."""
+        ms = np.zeros(1)
+        self._check(self.lib.ttdvm_cuda_round_resident(self.h, float(eps), int(cap), int(repeats),
+                                                       _ptr(ms)))
+        return float(ms[0])
+
+    def result(self) -> TtBatch:
+        """The result set of the last rounding call."""
+        n = self._last_nout
+        return self._fetch(n, lambda r, o: self.lib.ttdvm_cuda_result_layout(self.h, r, o),
+                           lambda c, cap_: self.lib.ttdvm_cuda_result_download(self.h, c, cap_))
 
     def compute_macro(self, b: TtBatch) -> np.ndarray:
         """Batched compute_macro: [count, 11] = n, u(3), T, rho, p, S(3), nu."""
