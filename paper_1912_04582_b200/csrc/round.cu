@@ -1276,15 +1276,15 @@ __global__ void __launch_bounds__(NT, SPILL ? 1 : (Q == 1 ? 6 : (Q == 3 ? 4 : (Q
     round_gram_kernel(RoundArgs p) {
   extern __shared__ double sm[];
   __shared__ int s_meta[8];
-  if (!SPILL) {
+  if constexpr (!SPILL) {
     const int o = p.olist ? p.olist[blockIdx.x] : blockIdx.x;
     if (o < p.nout) round_gram_body<Q, false>(p, o, sm, s_meta);
-    return;
-  }
-  for (int b = blockIdx.x; b < p.nblk; b += gridDim.x) {
-    const int o = p.olist ? p.olist[b] : b;
-    __syncthreads();  // the previous output's shared-memory readers are done
-    if (o < p.nout) round_gram_body<Q, true>(p, o, sm, s_meta);
+  } else {
+    for (int b = blockIdx.x; b < p.nblk; b += gridDim.x) {
+      const int o = p.olist ? p.olist[b] : b;
+      __syncthreads();  // the previous output's shared-memory readers are done
+      if (o < p.nout) round_gram_body<Q, true>(p, o, sm, s_meta);
+    }
   }
 }
 
