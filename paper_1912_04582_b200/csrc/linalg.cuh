@@ -413,5 +413,227 @@ __device__ __noinline__ int svd_from_r(const double* R, int ldr, int k, int m, c
   return t;
 }
 
+// ---- single-warp small-matrix routines ------------------------------------
+// The sequential factorizations of a rounding (pivoted Cholesky, one-sided
+// Jacobi) on Gram dimensions d <= 32 run on warp 0 alone with warp-level
+// synchronisation: each column step costs a few shuffles instead of three
+// block barriers, and the other warps of the CTA wait at ONE barrier after
+// the call (other CTAs keep the SM busy).  Same arithmetic as the block
+// versions, same results.
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWarpMaxD = 16;  // measured: the block versions win from ~24 up
+
+// chol_piv_dd on warp 0 (d <= 32): lane v holds virtual column v's pivot;
+// row k of R is formed by lane v (> k) and broadcast by shuffles for the
+// trailing update.  Caller: if (threadIdx.x < 32) k = ...; then a barrier.
+__device__ __noinline__ int chol_piv_dd_warp(double* Gh, double* Gl, int d, double thresh,
+                                             double* R, int ldr, int* piv) {
+  const int lane = threadIdx.x & 31;
+  int mp = lane;  // original index of virtual column `lane`
+  int k = 0;
+  for (; k < d; ++k) {
+    double bv = -1.0;
+    int bi = k;
+    if (lane >= k && lane < d) {
+      bv = Gh[mp + d * mp];
+      bi = lane;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, bv, o);
+      const int oi = __shfl_xor_sync(kFull, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (!(bv > thresh)) break;  // uniform
+    const int pk_old = __shfl_sync(kFull, mp, k);
+    const int pk = __shfl_sync(kFull, mp, bi);
+    if (lane == k) mp = pk;
+    else if (lane == bi) mp = pk_old;
+    if (bi != k && lane < k) {  // earlier rows of R follow the column swap
+      const double a = R[lane + ldr * k];
+      R[lane + ldr * k] = R[lane + ldr * bi];
+      R[lane + ldr * bi] = a;
+    }
+    const double ah = Gh[pk + d * pk], al = Gl[pk + d * pk];
+    const double s = sqrt(ah);
+    const double p0 = s * s, pe0 = fma(s, s, -p0);
+    const double r0 = ((ah - p0) - pe0 + al) * (0.5 / s);
+    double rh, rl;
+    two_sum(s, r0, rh, rl);
+    const double rinv = 1.0 / rh;
+    double qh = 0.0, ql = 0.0;
+    const bool act = lane > k && lane < d;
+    if (act) {
+      const double gh = Gh[pk + d * mp], gl = Gl[pk + d * mp];
+      const double q1 = gh * rinv;
+      double p, pe;
+      dd_mul(q1, 0.0, rh, rl, p, pe);
+      const double res = ((gh - p) - pe) + gl;
+      two_sum(q1, res * rinv, qh, ql);
+      R[k + ldr * lane] = qh + ql;
+    }
+    if (lane == k) R[k + ldr * k] = rh + rl;
+    // trailing update G[p_i, p_j] -= R_ki R_kj (i, j > k): lane j, loop over i
+    for (int i = k + 1; i < d; ++i) {
+      const double hi = __shfl_sync(kFull, qh, i), lo = __shfl_sync(kFull, ql, i);
+      const int pi = __shfl_sync(kFull, mp, i);
+      if (act) {
+        double p, pe;
+        dd_mul(hi, lo, qh, ql, p, pe);
+        const int e = pi + d * mp;
+        double sh_, e_;
+        two_sum(Gh[e], -p, sh_, e_);
+        double l2 = Gl[e] + e_ - pe;
+        dd_norm(sh_, l2);
+        Gh[e] = sh_;
+        Gl[e] = l2;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane < d) piv[lane] = mp;
+  __syncwarp();
+  return k;
+}
+
+// jacobi_t on warp 0 (c <= 32 columns): TPP lanes per pair.
+template <int TPP>
+__device__ int jacobi_warp_t(double* X, int ldx, int m, int c, double* nrm) {
+  const int lane = threadIdx.x & 31;
+  const int cp = c + (c & 1);
+  const int npairs = cp / 2;
+  const int pi = lane / TPP, sub = lane % TPP;
+  const double tol2 = 1e-30;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    for (int j = lane; j < c; j += 32) {
+      double s0 = 0.0, s1 = 0.0;
+      int i = 0;
+#pragma unroll 1
+      for (; i + 1 < m; i += 2) {
+        s0 += X[i + ldx * j] * X[i + ldx * j];
+        s1 += X[i + 1 + ldx * j] * X[i + 1 + ldx * j];
+      }
+      if (i < m) s0 += X[i + ldx * j] * X[i + ldx * j];
+      nrm[j] = s0 + s1;
+    }
+    __syncwarp();
+    bool rotated = false, big = false;
+    for (int r = 0; r < cp - 1; ++r) {
+      for (int base = 0; base < npairs; base += 32 / TPP) {
+        const int pp = base + pi;
+        int a = pp + r - 1;
+        if (a >= cp - 1) a -= cp - 1;
+        a = pp == 0 ? 0 : a + 1;
+        int b = cp - 2 - pp + r;
+        if (b >= cp - 1) b -= cp - 1;
+        b += 1;
+        const bool live = pp < npairs && a < c && b < c;
+        double ga = 0.0;
+        double* x = X + ldx * (live ? a : 0);
+        double* y = X + ldx * (live ? b : 0);
+        if (live)
+#pragma unroll 1
+          for (int i = sub; i < m; i += TPP) ga += x[i] * y[i];
+        ga = group_sum<TPP>(ga);
+        if (live && ga != 0.0) {
+          const double al = nrm[a], be = nrm[b];
+          if (ga * ga > tol2 * al * be) {
+            big = big || (ga * ga > 1e-18 * al * be);
+            const double dlt = be - al;
+            const double mag = fmax(fabs(dlt), 2.0 * fabs(ga));
+            const int ex = (int)((__double_as_longlong(mag) >> 52) & 0x7ff) - 1023;
+            const double sc = __longlong_as_double((long long)(1023 - ex) << 52);
+            const float df = (float)(dlt * sc), gf = (float)(ga * sc);
+            const float tf = copysignf(1.0f, df) * (2.0f * gf) /
+                             (fabsf(df) + sqrtf(df * df + 4.0f * gf * gf));
+            const double t = (double)tf;
+            rotated = rotated || (tf != 0.0f);
+            const double cs = fast_rsqrt(1.0 + t * t), sn = cs * t;
+#pragma unroll 1
+            for (int i = sub; i < m; i += TPP) {
+              const double xi = x[i], yi = y[i];
+              x[i] = cs * xi - sn * yi;
+              y[i] = sn * xi + cs * yi;
+            }
+            if (sub == 0) {
+              const double c2 = cs * cs, tg = 2.0 * t * ga, t2 = t * t;
+              nrm[a] = c2 * (al - tg + t2 * be);
+              nrm[b] = c2 * (be + tg + t2 * al);
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (!__any_sync(kFull, rotated) || !__any_sync(kFull, big)) return sweep + 1;
+  }
+  return 60;
+}
+
+__device__ __noinline__ int jacobi_warp(double* X, int ldx, int m, int c, double* nrm) {
+  const int npairs = (c + 1) / 2;
+  const int tpp = min(32, floor_pow2(max(1, 32 / max(npairs, 1))));
+  switch (tpp) {
+    case 32: return jacobi_warp_t<32>(X, ldx, m, c, nrm);
+    case 16: return jacobi_warp_t<16>(X, ldx, m, c, nrm);
+    case 8: return jacobi_warp_t<8>(X, ldx, m, c, nrm);
+    case 4: return jacobi_warp_t<4>(X, ldx, m, c, nrm);
+    case 2: return jacobi_warp_t<2>(X, ldx, m, c, nrm);
+    default: return jacobi_warp_t<1>(X, ldx, m, c, nrm);
+  }
+}
+
+// svd_from_r on warp 0 (k <= 32); t is returned to every lane of warp 0.
+__device__ __noinline__ int svd_from_r_warp(const double* R, int ldr, int k, int m, const int* piv,
+                                            const SvdWork& w, double budget2, int cap, double* U,
+                                            int ldu, double* margin_out) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < m * k; e += 32) {
+    const int r = e / m, i = e - r * m;
+    w.Xs[i + w.ldx * r] = i >= r ? R[r + ldr * i] : 0.0;
+  }
+  __syncwarp();
+  const int sweeps = jacobi_warp(w.Xs, w.ldx, m, k, w.vn);
+  if (w.prof && lane == 0) {
+    atomicAdd(&w.prof[12], (unsigned long long)sweeps);
+    atomicAdd(&w.prof[13], 1ULL);
+    if (sweeps >= 60) atomicAdd(&w.prof[14], 1ULL);
+  }
+  double v = 0.0;
+  if (lane < k) {
+    double s0 = 0.0, s1 = 0.0;
+    int i = 0;
+    for (; i + 1 < m; i += 2) {
+      s0 += w.Xs[i + w.ldx * lane] * w.Xs[i + w.ldx * lane];
+      s1 += w.Xs[i + 1 + w.ldx * lane] * w.Xs[i + 1 + w.ldx * lane];
+    }
+    if (i < m) s0 += w.Xs[i + w.ldx * lane] * w.Xs[i + w.ldx * lane];
+    v = sqrt(s0 + s1);
+  }
+  // descending rank of lane's value (ties: lower index first)
+  int rank = 0;
+  for (int o = 0; o < k; ++o) {
+    const double u = __shfl_sync(kFull, v, o);
+    rank += (u > v) || (u == v && o < lane);
+  }
+  if (lane < k) {
+    w.sig[rank] = v;
+    w.perm[rank] = lane;
+  }
+  __syncwarp();
+  int t = 0;
+  if (lane == 0) t = truncation_rank(w.sig, k, budget2, cap, margin_out);
+  t = __shfl_sync(kFull, t, 0);
+  for (int e = lane; e < m * t; e += 32) {
+    const int r = e / m, i = e - r * m;
+    U[piv[i] + ldu * r] = w.Xs[i + w.ldx * w.perm[r]] / w.sig[r];
+  }
+  __syncwarp();
+  return t;
+}
+
 }  // namespace
 }  // namespace ttdvm

@@ -183,6 +183,73 @@ __device__ __noinline__ void qr_inplace(double* A, int lda, int m, int ncols, do
   }
 }
 
+// qr_inplace with one barrier per column step: a group of TPC threads owns
+// each column (c * TPC <= NT) and its rows (sub, sub + TPC, ...); the owner
+// of column k forms its reflector (larfg, scaled tail in place) while the
+// other groups are still updating for step k - 1, and learns its squared
+// norm while applying step k - 1.  Same reflector format as qr_inplace.
+template <int TPC>
+__device__ void qr_grp_t(double* A, int lda, int m, int c, double* tau, double* sh) {
+  const int g = threadIdx.x / TPC, sub = threadIdx.x % TPC;
+  const int kmax = min(m, c);
+  const bool own = g < c;
+  double* col = A + lda * (own ? g : 0);
+  double s2 = 0.0;
+  if (g == 0 && own)
+    for (int i = 1 + sub; i < m; i += TPC) s2 += col[i] * col[i];
+  s2 = group_sum<TPC>(s2);
+  for (int k = 0; k < kmax; ++k) {
+    if (g == k) {  // reflector of column k (rows > k), alpha from the row-k owner
+      double beta, t, sc;
+      larfg(col[k], s2, beta, t, sc);  // row k: visible to the group since the last __syncwarp
+      if (t != 0.0) {
+        for (int i = k + 1 + ((sub - k - 1) % TPC + TPC) % TPC; i < m; i += TPC) col[i] *= sc;
+        if (sub == 0) col[k] = beta;
+      }
+      if (sub == 0) {
+        tau[k] = t;
+        sh[k & 1] = t;
+      }
+    }
+    __syncthreads();
+    const double t = sh[k & 1];
+    const bool act = own && g > k && t != 0.0;
+    const double* v = A + lda * k;
+    double w = 0.0;
+    const int i0 = k + 1 + ((sub - k - 1) % TPC + TPC) % TPC;  // first own row > k
+    if (act)
+      for (int i = i0; i < m; i += TPC) w += v[i] * col[i];
+    w = group_sum<TPC>(w);
+    double ss = 0.0;
+    if (act) {
+      w = t * (w + col[k]);
+      for (int i = i0; i < m; i += TPC) {
+        const double x = col[i] - w * v[i];
+        col[i] = x;
+        if (i > k + 1) ss += x * x;
+      }
+    } else if (own && g == k + 1) {
+      for (int i = i0; i < m; i += TPC)
+        if (i > k + 1) ss += col[i] * col[i];
+    }
+    ss = group_sum<TPC>(ss);
+    if (g == k + 1) s2 = ss;
+    __syncwarp();  // every lane of the group has read row k
+    if (act && sub == 0) col[k] -= w;
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+__device__ __noinline__ void qr_grp(double* A, int lda, int m, int c, double* tau, double* sh) {
+  if (c * 32 <= NT) qr_grp_t<32>(A, lda, m, c, tau, sh);
+  else if (c * 16 <= NT) qr_grp_t<16>(A, lda, m, c, tau, sh);
+  else if (c * 8 <= NT) qr_grp_t<8>(A, lda, m, c, tau, sh);
+  else if (c * 4 <= NT) qr_grp_t<4>(A, lda, m, c, tau, sh);
+  else if (c * 2 <= NT) qr_grp_t<2>(A, lda, m, c, tau, sh);
+  else qr_grp_t<1>(A, lda, m, c, tau, sh);
+}
+
 // QR of [R; B] -> R, R upper c x c (ld ldr), B h x c (ld ldb) read once.
 // Groups of TPC threads own one column each (c <= NT / TPC) and keep its
 // rows (sub, sub + TPC, ...) in registers; the Householder vector of step k
@@ -610,6 +677,32 @@ __device__ void times_r3t_b(double* out, int ldo, int os, const double* X, int l
   });
 }
 
+// Block or single-warp pivoted dd Cholesky / svd_from_r by size; results
+// (rank, truncation) broadcast to the CTA through s_int.
+__device__ __forceinline__ int chol_any(double* Gh, double* Gl, int d, double thresh, double* R,
+                                        int ldr, int* piv, double* sh, int* s_int) {
+  if (d > kWarpMaxD) return chol_piv_dd(Gh, Gl, d, thresh, R, ldr, piv, sh);
+  if (threadIdx.x < 32) {
+    const int k = chol_piv_dd_warp(Gh, Gl, d, thresh, R, ldr, piv);
+    if (threadIdx.x == 0) *s_int = k;
+  }
+  __syncthreads();
+  return *s_int;
+}
+
+__device__ __forceinline__ int svd_r_any(const double* R, int ldr, int k, int m, const int* piv,
+                                         const SvdWork& w, double budget2, int cap, double* U,
+                                         int ldu, double* margin_out, int* s_int) {
+  if (k > kWarpMaxD)
+    return svd_from_r(R, ldr, k, m, piv, w, budget2, cap, U, ldu, margin_out, s_int);
+  if (threadIdx.x < 32) {
+    const int t = svd_from_r_warp(R, ldr, k, m, piv, w, budget2, cap, U, ldu, margin_out);
+    if (threadIdx.x == 0) *s_int = t;
+  }
+  __syncthreads();
+  return *s_int;
+}
+
 template <int Q>
 __device__ __forceinline__ void gram_rows_acc(double (&gh)[Q], double (&gl)[Q], const int (&ei)[Q],
                                               const int (&ej)[Q], const double* T, int ldt,
@@ -1006,7 +1099,11 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
   materialise_outer(F, lastT, terms, K, n1, n2, n3);
   __syncthreads();
   PROF(0);
-  qr_inplace(lastT, n3, n3, R2, tau, sh);
+  if (R2 <= NT) {
+    qr_grp(lastT, n3, n3, R2, tau, sh);
+  } else {
+    qr_inplace(lastT, n3, n3, R2, tau, sh);
+  }
   const int q3 = min(n3, R2);
   PROF(1);
 
@@ -1072,7 +1169,7 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
   double norm2 = trace;
   int k1 = 0;
   if (wroute && trace > 0.0 && isfinite(trace)) {
-    k1 = chol_piv_dd(G, Gl, d1, 1e-31 * trace, Rc, D, piv, sh);
+    k1 = chol_any(G, Gl, d1, 1e-31 * trace, Rc, D, piv, sh, &s_meta[6]);
     // M = C^T (k1 x n1, ld D1) into Tb: M(r, i) = sum_{v >= r} R_W(r, v) F(i, piv[v])
     double l2 = 0.0;
     for2d(k1, n1, [&](int r, int i) {
@@ -1115,13 +1212,47 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
   const SvdWork sw{p.prof, Xs, vn, sig, sraw, piv, perm, sh, mx};
   double mg1 = 0.0;
   int t1;
-  if (wroute) {
+  if (wroute && k1 <= kWarpMaxD) {
+    // sigma and U1 of C (n1 x k1, C^T in Tb) through its k1 x k1 Gram:
+    // exact dd Gram -> pivoted dd Cholesky Rg -> Jacobi on Rg^T gives sigma
+    // and the right vectors V (into XP, k1 x t1); U1 = C V / sigma.  The
+    // retained sigma are >= eps ||A|| / sqrt(2), so U1 carries at most
+    // ~u / eps relative error; the rank decisions see sigma to ~u ||A||.
+    PROF(3);
+    {
+      const int ne = k1 * (k1 + 1) / 2;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int e = threadIdx.x + NT * q;
+        gh[q] = gl[q] = 0.0;
+        if (e < ne) tri_index(e, k1, ei[q], ej[q]);
+        else ei[q] = ej[q] = -1;
+      }
+    }
+    gram_rows_acc<Q>(gh, gl, ei, ej, Tb, D1, n1);
+    gram_store<Q>(G, Gl, k1, gh, gl, ei, ej);
+    __syncthreads();
+    const int kc = chol_any(G, Gl, k1, cthresh, Rc, D, piv, sh, &s_meta[6]);
+    double* V = XP;  // k1 x t1
+    t1 = svd_r_any(Rc, D, kc, k1, piv, sw, budget2, p.cap, V, k1, &mg1, &s_meta[4]);
+    for2d(n1, t1, [&](int i, int r) {
+      double a0 = 0.0, a1 = 0.0;
+      int v = 0;
+      for (; v + 1 < k1; v += 2) {
+        a0 += Tb[v + D1 * i] * V[v + k1 * r];
+        a1 += Tb[v + 1 + D1 * i] * V[v + 1 + k1 * r];
+      }
+      if (v < k1) a0 += Tb[v + D1 * i] * V[v + k1 * r];
+      U1[i + n1 * r] = (a0 + a1) / sig[r];
+    });
+    __syncthreads();
+  } else if (wroute) {
     PROF(3);
     t1 = svd_left(Tb, D1, k1, n1, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
   } else {
-    k1 = chol_piv_dd(G, Gl, n1, cthresh, Rc, D, piv, sh);
+    k1 = chol_any(G, Gl, n1, cthresh, Rc, D, piv, sh, &s_meta[6]);
     PROF(3);
-    t1 = svd_from_r(Rc, D, k1, n1, piv, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
+    t1 = svd_r_any(Rc, D, k1, n1, piv, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
   }
   if (p.margins && threadIdx.x == 0) p.margins[2 * o] = mg1;
   PROF(5);
@@ -1169,11 +1300,11 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
   gram_store<Q>(G, Gl, q3, gh, gl, ei, ej);
   __syncthreads();
   PROF(6);
-  const int k2 = chol_piv_dd(G, Gl, q3, cthresh, Rc, D, piv, sh);
+  const int k2 = chol_any(G, Gl, q3, cthresh, Rc, D, piv, sh, &s_meta[6]);
   PROF(7);
   double mg2 = 0.0;
   double* W2 = Tb;  // V2 (q3 x t2), ld D3
-  const int t2 = svd_from_r(Rc, D, k2, q3, piv, sw, budget2, p.cap, W2, D3, &mg2, &s_meta[5]);
+  const int t2 = svd_r_any(Rc, D, k2, q3, piv, sw, budget2, p.cap, W2, D3, &mg2, &s_meta[5]);
   PROF(9);
   if (threadIdx.x == 0) {
     if (p.margins) p.margins[2 * o + 1] = mg2;
