@@ -381,12 +381,13 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   a.acc = c->d_acc.p;
   a.prof = c->round_prof ? c->d_prof.p : nullptr;
   // rank bins: per-bin shared-memory plans (one tiny kernel + readback)
-  c->d_bins.alloc((size_t)kRankBins * 5);
+  constexpr int kBinAll = kRankBins * (1 + kBinWords);
+  c->d_bins.alloc((size_t)kBinAll);
   c->d_olist.alloc((size_t)kRankBins * nout);
-  CK(cudaMemsetAsync(c->d_bins.p, 0, kRankBins * 5 * sizeof(int), c->st));
+  CK(cudaMemsetAsync(c->d_bins.p, 0, kBinAll * sizeof(int), c->st));
   CK(launch_round_bins(a, c->d_bins.p, c->d_bins.p + kRankBins, c->d_olist.p, c->st));
   c->launches += 1;
-  int hb[kRankBins * 5];
+  int hb[kBinAll];
   CK(cudaMemcpyAsync(hb, c->d_bins.p, sizeof(hb), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   const int* bcount = hb;
@@ -394,9 +395,9 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   int RM1 = 1, RM2 = 1, MSMAX = 1;
   for (int b = 0; b < kRankBins; ++b) {
     if (!bcount[b]) continue;
-    RM1 = std::max(RM1, bmax[4 * b]);
-    RM2 = std::max(RM2, bmax[4 * b + 1]);
-    MSMAX = std::max(MSMAX, bmax[4 * b + 2]);
+    RM1 = std::max(RM1, bmax[kBinWords * b]);
+    RM2 = std::max(RM2, bmax[kBinWords * b + 1]);
+    MSMAX = std::max(MSMAX, bmax[kBinWords * b + 2]);
   }
   const int mx = n;
   // exact-Gram route by default; TTDVM_ROUND=tsqr selects the Householder
@@ -417,33 +418,42 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     int bin, count, rm1, rm2, ms, jb;
     bool spill;
   };
+  // CTAs per SM the kernel variant is built for (launch bounds by Gram size)
+  auto blocks_per_sm = [&](int rm1, int rm2) {
+    const int d = std::max(std::min(n, rm1), std::min(n, rm2));
+    const int ne = d * (d + 1) / 2;
+    return ne <= 3 * kRoundThreads ? 4 : (ne <= 10 * kRoundThreads ? 3 : 1);
+  };
   // slices per barrier phase: about a quarter of the slices (measured best
   // on config 4: fewer phases pay for a lower CTA count), shrunk while the
-  // plan would leave fewer than 3 CTAs per SM
-  auto pick_jb = [&](int rm1, int rm2, int ms) {
-    const size_t base = round_gram_smem_bytes(n, n, rm1, rm2, ms, 1, false);
-    const size_t budget = std::max(base, (size_t)(228 * 1024 / 3) - 2048);
+  // plan would leave fewer CTAs per SM than the variant's launch bounds
+  auto pick_jb = [&](const Launch& l) {
+    const size_t base = round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false);
+    const size_t budget =
+        std::max(base, (size_t)(228 * 1024 / blocks_per_sm(l.rm1, l.rm2)) - 2048);
     int jb = (n + 3) / 4;
-    while (jb > 1 && round_gram_smem_bytes(n, n, rm1, rm2, ms, jb, false) > budget) --jb;
+    while (jb > 1 && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, jb, false) > budget) --jb;
     return jb;
   };
   std::vector<Launch> plan;
   for (int b = kRankBins - 1; b >= 0; --b) {  // large ranks first (long CTAs start early)
     if (!bcount[b]) continue;
-    Launch l{b, bcount[b], std::max(1, bmax[4 * b]), std::max(1, bmax[4 * b + 1]),
-             std::max(1, bmax[4 * b + 2]), 1, false};
+    const int* bm = bmax + kBinWords * b;
+    Launch l{b, bcount[b], std::max(1, bm[0]), std::max(1, bm[1]), std::max(1, bm[2]), 1, false};
     // working sets above the shared-memory budget (n = 64, summed ranks of
     // ~100 and more) take the spill plan: F, last^T, XP and the Gram region
     // in a per-CTA global scratch slice, persistent CTAs
-    l.spill = !use_tsqr && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false) > kSmemMax;
-    l.jb = (use_tsqr || l.spill) ? 1 : pick_jb(l.rm1, l.rm2, l.ms);
+    l.spill = !use_tsqr &&
+              round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false) > kSmemMax;
+    if (!use_tsqr && !l.spill) l.jb = pick_jb(l);
     static const int force_jb = [] {  // diagnostics: TTDVM_JB=k forces k slices per phase
       const char* e = getenv("TTDVM_JB");
       return e ? atoi(e) : 0;
     }();
     if (force_jb > 0 && !use_tsqr && !l.spill) {
       l.jb = std::min(n, force_jb);
-      while (l.jb > 1 && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, l.jb, false) > kSmemMax)
+      while (l.jb > 1 &&
+             round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, l.jb, false) > kSmemMax)
         --l.jb;
     }
     if (l.spill && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, true) > kSmemMax)
@@ -458,6 +468,16 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   if (out.arena.n == 0) {
     const int re = std::min(n, 4);
     out.arena.alloc((size_t)nout * tt_size(n, n, n, re, re) + 1024);
+  } else {
+    // headroom: ranks drift upward from step to step; an arena that held
+    // this set's previous result with less than 25 % to spare is regrown
+    // before the launch (its content is dead), so the overflow-and-repeat
+    // path below stays rare
+    const size_t want = (size_t)((double)out.used * 1.25) + 1024;
+    if (out.arena.n < want) {
+      out.arena.free();
+      out.arena.alloc(want);
+    }
   }
   for (int attempt = 0; attempt < 4; ++attempt) {
     a.out.ranks = out.ranks.p;

@@ -45,7 +45,8 @@ struct TermInfo {
   int b1, b2, fa1, fa2;
 };
 
-// Resolve the summands of output o into TermInfo (thread 0) and the row /
+// Resolve the summands of output o into TermInfo (thread k reads term k;
+// thread 0 then forms the running offsets from shared memory) and the row /
 // column -> term maps.  A term's ranks are (fa1 b1, fa2 b2): the Hadamard
 // product fb o base (proj/src/tt_tensor.cpp:212-245) is never formed, its
 // Kronecker-structured cores are built on the fly where they are consumed.
@@ -54,42 +55,46 @@ __device__ void setup_terms(const RoundArgs& p, int o, TermInfo* terms, int* row
   const long long t0 = p.term_off ? p.term_off[o] : (long long)o;
   K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
   const int n1 = p.n1, n2 = p.n2, n3 = p.n3;
+  for (int k = threadIdx.x; k < K; k += NT) {
+    const Term tm = p.terms[t0 + k];
+    const TSet& s = p.sets[tm.set];
+    TermInfo ti;
+    ti.b1 = s.ranks[2 * tm.idx];
+    ti.b2 = s.ranks[2 * tm.idx + 1];
+    ti.base = s.base + s.off[tm.idx];
+    double sc = tm.scale * s.uscale;
+    if (s.tscale) sc *= s.tscale[tm.idx];
+    if (tm.dsi >= 0) sc *= p.dscale[tm.dsi];
+    ti.scale = sc;
+    ti.refl = tm.refl;
+    const double* fac = tm.fac >= 0 ? p.factors + (long long)tm.fac * (n1 + n2 + n3) : nullptr;
+    ti.u[0] = fac ? fac : nullptr;
+    ti.u[1] = fac ? fac + n1 : nullptr;
+    ti.u[2] = fac ? fac + n1 + n2 : nullptr;
+    if (tm.fset >= 0) {
+      const TSet& f = p.sets[tm.fset];
+      ti.fa1 = f.ranks[2 * tm.fidx];
+      ti.fa2 = f.ranks[2 * tm.fidx + 1];
+      ti.fb = f.base + f.off[tm.fidx];
+    } else {
+      ti.fa1 = ti.fa2 = 1;
+      ti.fb = nullptr;
+    }
+    ti.r1 = ti.fa1 * ti.b1;
+    ti.r2 = ti.fa2 * ti.b2;
+    terms[k] = ti;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     int off1 = 0, off2 = 0, ms = 0;
     for (int k = 0; k < K; ++k) {
-      const Term tm = p.terms[t0 + k];
-      const TSet& s = p.sets[tm.set];
-      TermInfo ti;
-      ti.b1 = s.ranks[2 * tm.idx];
-      ti.b2 = s.ranks[2 * tm.idx + 1];
-      ti.base = s.base + s.off[tm.idx];
-      double sc = tm.scale * s.uscale;
-      if (s.tscale) sc *= s.tscale[tm.idx];
-      if (tm.dsi >= 0) sc *= p.dscale[tm.dsi];
-      ti.scale = sc;
-      ti.refl = tm.refl;
-      const double* fac = tm.fac >= 0 ? p.factors + (long long)tm.fac * (n1 + n2 + n3) : nullptr;
-      ti.u[0] = fac ? fac : nullptr;
-      ti.u[1] = fac ? fac + n1 : nullptr;
-      ti.u[2] = fac ? fac + n1 + n2 : nullptr;
-      if (tm.fset >= 0) {
-        const TSet& f = p.sets[tm.fset];
-        ti.fa1 = f.ranks[2 * tm.fidx];
-        ti.fa2 = f.ranks[2 * tm.fidx + 1];
-        ti.fb = f.base + f.off[tm.fidx];
-      } else {
-        ti.fa1 = ti.fa2 = 1;
-        ti.fb = nullptr;
-      }
-      ti.r1 = ti.fa1 * ti.b1;
-      ti.r2 = ti.fa2 * ti.b2;
-      ti.off1 = off1;
-      ti.off2 = off2;
-      ti.ms = ms;
-      off1 += ti.r1;
-      off2 += ti.r2;
-      ms += ti.r1 * ti.r2;
-      terms[k] = ti;
+      TermInfo& t = terms[k];
+      t.off1 = off1;
+      t.off2 = off2;
+      t.ms = ms;
+      off1 += t.r1;
+      off2 += t.r2;
+      ms += t.r1 * t.r2;
     }
     s_meta[0] = off1;
     s_meta[1] = off2;
@@ -1132,8 +1137,10 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
     for (int j0 = 0; j0 < n2; j0 += JB) {
       const int jn = min(JB, n2 - j0);
       __syncthreads();
+      PROF(2);
       stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
       __syncthreads();
+      PROF(11);
       // Z_j^T: Tb(a, (jj, c)) = sum_b M_t(a, b) R3(c, off2 + b), R3 upper trapezoidal
       for2d(R1, jn * q3, [&](int a, int jc) {
         const int jj = jc / q3, c = jc - jj * q3;
@@ -1145,6 +1152,7 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
         Tb[a + d1 * jc] = s;
       });
       __syncthreads();
+      PROF(4);
       gram_rows_acc<Q>(gh, gl, ei, ej, Tb, d1, jn * q3);
     }
   } else {
@@ -1285,15 +1293,18 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
     const int jn = min(JB, n2 - j0);
     double* X2j = keepX2 ? X2 + j0 * t1 * R2 : X2;
     __syncthreads();
+    PROF(6);
     if (!staged_all) {
       stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
       __syncthreads();
     }
+    PROF(11);
     left_times_blockdiag_b(X2j, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn);
     __syncthreads();
     // S_j^T (q3 x t1) at column block jj
     times_r3t_b(Tb, q3, q3 * t1, X2j, t1, t1 * R2, t1, q3, R2, lastT, n3, jn);
     __syncthreads();
+    PROF(8);
     gram_rows_acc<Q>(gh, gl, ei, ej, Tb, q3, jn * t1);
   }
   __syncthreads();
@@ -1403,7 +1414,7 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
 // Shared-memory plans: one CTA per output (6 / 4 / 3 CTAs per SM by Gram
 // size); SPILL launches are persistent (grid = resident CTAs) and loop.
 template <int Q, bool SPILL>
-__global__ void __launch_bounds__(NT, SPILL ? 1 : (Q == 1 ? 6 : (Q == 3 ? 4 : (Q <= 10 ? 3 : 1))))
+__global__ void __launch_bounds__(NT, SPILL ? 1 : (Q <= 3 ? 4 : (Q <= 10 ? 3 : 1)))
     round_gram_kernel(RoundArgs p) {
   extern __shared__ double sm[];
   __shared__ int s_meta[8];
@@ -1537,10 +1548,10 @@ __global__ void round_bin_kernel(RoundArgs p, int* counts, int* bmax, int* lists
     while (bin < kRankBins - 1 && key > kRankEdges[bin]) ++bin;
     const int pos = atomicAdd(&counts[bin], 1);
     lists[(long long)bin * p.nout + pos] = o;
-    atomicMax(&bmax[4 * bin], r1);
-    atomicMax(&bmax[4 * bin + 1], r2);
-    atomicMax(&bmax[4 * bin + 2], ms);
-    atomicMax(&bmax[4 * bin + 3], K);
+    atomicMax(&bmax[kBinWords * bin], r1);
+    atomicMax(&bmax[kBinWords * bin + 1], r2);
+    atomicMax(&bmax[kBinWords * bin + 2], ms);
+    atomicMax(&bmax[kBinWords * bin + 3], K);
   }
 }
 

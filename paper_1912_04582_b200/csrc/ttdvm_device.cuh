@@ -12,6 +12,9 @@ constexpr int kAccSlots = 64;     // spread slots of the per-launch work counter
 constexpr int kRoundThreads = 128;
 // rank bins of a rounding launch: upper edges of max(R1, R2) of the summed input
 constexpr int kRankBins = 11;
+// per-bin maxima written by the bin kernel: R1, R2, staged-slice doubles,
+// summands
+constexpr int kBinWords = 4;
 __device__ __constant__ const int kRankEdges[kRankBins] = {4, 8, 12, 16, 24, 32, 48, 64, 96, 128,
                                                            1 << 30};
 

@@ -20,7 +20,8 @@ import numpy as np
 from .tt_batch import TtBatch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libttdvm_cuda.so")
+# TTDVM_LIB overrides the library path (A/B measurements of alternative builds)
+LIB_PATH = os.environ.get("TTDVM_LIB") or os.path.join(HERE, "libttdvm_cuda.so")
 
 # every symbol declared in include/ttdvm_cuda.h
 EXPORTS = (

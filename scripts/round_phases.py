@@ -13,8 +13,9 @@ import numpy as np  # noqa: E402
 
 from paper_1912_04582_b200.cuda import Context  # noqa: E402
 
-NAMES = {0: "load", 1: "qr_last", 2: "cut1_gram", 3: "chol1(+C)", 5: "svd1", 6: "P+cut2_gram",
-         7: "chol2", 9: "svd2", 10: "output"}
+NAMES = {0: "load", 1: "qr_last", 11: "stage_slices", 4: "cut1_Zj", 2: "cut1_gram_acc",
+         3: "chol1(+C)", 5: "svd1", 8: "cut2_X2_S", 6: "P+cut2_gram_acc", 7: "chol2", 9: "svd2",
+         10: "output"}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
