@@ -45,6 +45,14 @@ struct TermInfo {
   int b1, b2, fa1, fa2;
 };
 
+// prefetch.global.L1 of the 128-byte lines covering [p, p + count)
+__device__ __forceinline__ void prefetch_l1(const double* p, long long count) {
+  const unsigned long long a0 = reinterpret_cast<unsigned long long>(p) & ~127ull;
+  const unsigned long long a1 = reinterpret_cast<unsigned long long>(p + count);
+  for (unsigned long long a = a0 + 128ull * threadIdx.x; a < a1; a += 128ull * NT)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+}
+
 // Resolve the summands of output o into TermInfo (thread k reads term k;
 // thread 0 then forms the running offsets from shared memory) and the row /
 // column -> term maps.  A term's ranks are (fa1 b1, fa2 b2): the Hadamard
@@ -106,6 +114,16 @@ __device__ void setup_terms(const RoundArgs& p, int o, TermInfo* terms, int* row
     const TermInfo& t = terms[k];
     for (int a = threadIdx.x; a < t.r1; a += NT) rowterm[t.off1 + a] = k;
     for (int b = threadIdx.x; b < t.r2; b += NT) colterm[t.off2 + b] = k;
+  }
+  // Pull every summand's cores (and Hadamard factor cores) toward L1 now:
+  // the slice stages of both cuts and the output read them many phases
+  // later, and their loads sit on the critical path of each phase.
+  for (int k = 0; k < K; ++k) {
+    const TermInfo& t = terms[k];
+    const long long nb = (long long)n1 * t.b1 + (long long)n2 * t.b1 * t.b2 + (long long)t.b2 * n3;
+    prefetch_l1(t.base, nb);
+    if (t.fb)
+      prefetch_l1(t.fb, (long long)n1 * t.fa1 + (long long)n2 * t.fa1 * t.fa2 + (long long)t.fa2 * n3);
   }
 }
 
@@ -604,26 +622,36 @@ __device__ void times_r3t(double* out, int ldo, bool trans, const double* X, int
 // threads stay busy when the per-slice blocks are small ----
 __device__ void stage_slices(double* Ms, int msld, const TermInfo* terms, int K, int n1, int n2,
                              int j0, int jn) {
+  // a thread keeps one in-slice element r (its Kronecker indices are formed
+  // once) and walks the slices jj: no integer division in the loop
   for (int k = 0; k < K; ++k) {
     const TermInfo& t = terms[k];
-    const int sz = t.r1 * t.r2;
-    for (int e = threadIdx.x; e < jn * sz; e += NT) {
-      const int jj = e / sz, r = e - jj * sz;
-      const int j = j0 + jj;
-      const int jr = t.refl == 2 ? n2 - 1 - j : j;
-      const double* src = t.base + (long long)n1 * t.b1 + (long long)jr * t.b1 * t.b2;
-      const double f = t.u[1] ? t.u[1][j] : 1.0;
-      double v;
-      if (!t.fb) {
-        v = f * src[r];
-      } else {  // Kronecker block A2_j (x) B2_j: (p*b1 + q, p'*b2 + q') = A(p,p') B(q,q')
-        const double* fs = t.fb + (long long)n1 * t.fa1 + (long long)j * t.fa1 * t.fa2;
-        const int c = r / t.r1, a = r - c * t.r1;
-        const int p = a / t.b1, q = a - p * t.b1;
-        const int pp = c / t.b2, qq = c - pp * t.b2;
-        v = f * fs[p + t.fa1 * pp] * src[q + t.b1 * qq];
+    const int r1 = t.r1, sz = r1 * t.r2, b1 = t.b1, b2 = t.b2, fa1 = t.fa1, fa2 = t.fa2;
+    const int lg = sz <= 1 ? 0 : min(LOG_NT, 32 - __clz(sz - 1));
+    const int step = NT >> lg;
+    const double* mb = t.base + (long long)n1 * b1;
+    const double* mf = t.fb ? t.fb + (long long)n1 * fa1 : nullptr;
+    const double* u1 = t.u[1];
+    const bool rev = t.refl == 2;
+    double* dst = Ms + t.ms;
+    for (int r = threadIdx.x & ((1 << lg) - 1); r < sz; r += 1 << lg) {
+      int os = r, of = 0;
+      if (mf) {  // Kronecker block A2_j (x) B2_j: (p*b1 + q, p'*b2 + q') = A(p,p') B(q,q')
+        const int c = r / r1, a = r - c * r1;
+        const int pa = a / b1, q = a - pa * b1;
+        const int pc = c / b2, qq = c - pc * b2;
+        os = q + b1 * qq;
+        of = pa + fa1 * pc;
       }
-      Ms[jj * msld + t.ms + r] = v;
+#pragma unroll 1
+      for (int jj = threadIdx.x >> lg; jj < jn; jj += step) {
+        const int j = j0 + jj;
+        const int jr = rev ? n2 - 1 - j : j;
+        double v = mb[(long long)jr * b1 * b2 + os];
+        if (mf) v *= mf[(long long)j * fa1 * fa2 + of];
+        if (u1) v *= u1[j];
+        dst[jj * msld + r] = v;
+      }
     }
   }
 }
@@ -1093,11 +1121,16 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
       reinterpret_cast<double*>(rowterm + RM1 + (((RM1 + RM2) & 1) ? 1 : 0)));
 
   long long prof_t = p.prof ? clock64() : 0;
+  // diagnostics: per-phase cycles of thread 0, with a barrier first so a
+  // phase is charged to the phase that did the work (profiling runs only)
 #define PROF(k)                                                      \
-  if (p.prof && threadIdx.x == 0) {                                  \
-    const long long t_ = clock64();                                  \
-    atomicAdd(&p.prof[k], (unsigned long long)(t_ - prof_t));        \
-    prof_t = t_;                                                     \
+  if (p.prof) {                                                      \
+    __syncthreads();                                                 \
+    if (threadIdx.x == 0) {                                          \
+      const long long t_ = clock64();                                \
+      atomicAdd(&p.prof[k], (unsigned long long)(t_ - prof_t));      \
+      prof_t = t_;                                                   \
+    }                                                                \
   }
   int K, R1, R2;
   setup_terms(p, o, terms, rowterm, colterm, s_meta, K, R1, R2);
@@ -1141,16 +1174,34 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
       stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
       __syncthreads();
       PROF(11);
-      // Z_j^T: Tb(a, (jj, c)) = sum_b M_t(a, b) R3(c, off2 + b), R3 upper trapezoidal
-      for2d(R1, jn * q3, [&](int a, int jc) {
-        const int jj = jc / q3, c = jc - jj * q3;
-        const TermInfo& t = terms[rowterm[a]];
-        const int aa = a - t.off1;
-        const double* mj = Ms + jj * p.MSMAX + t.ms + aa;
-        double s = 0.0;
-        for (int b = max(0, c - t.off2); b < t.r2; ++b) s += lastT[c + n3 * (t.off2 + b)] * mj[t.r1 * b];
-        Tb[a + d1 * jc] = s;
-      });
+      // Z_j^T: Tb(a, (jj, c)) = sum_b M_t(a, b) R3(c, off2 + b), R3 upper
+      // trapezoidal.  Row a is fixed per thread (its term is looked up once);
+      // (jj, c) advance without division.
+      {
+        const int lg = R1 <= 1 ? 0 : min(LOG_NT, 32 - __clz(R1 - 1));
+        const int a = threadIdx.x & ((1 << lg) - 1), step = NT >> lg;
+        const int ncol = jn * q3;
+        for (int a2 = a; a2 < R1; a2 += (1 << lg)) {
+          const TermInfo& t = terms[rowterm[a2]];
+          const int r1 = t.r1, r2 = t.r2, off2 = t.off2;
+          const double* mbase = Ms + t.ms + (a2 - t.off1);
+          const double* lb = lastT + n3 * off2;
+          int jc = threadIdx.x >> lg;
+          int jj = jc / q3, c = jc - jj * q3;
+#pragma unroll 1
+          for (; jc < ncol; jc += step) {
+            const double* mj = mbase + jj * p.MSMAX;
+            double s = 0.0;
+            for (int b = max(0, c - off2); b < r2; ++b) s += lb[c + n3 * b] * mj[r1 * b];
+            Tb[a2 + d1 * jc] = s;
+            c += step;
+            while (c >= q3) {
+              c -= q3;
+              ++jj;
+            }
+          }
+        }
+      }
       __syncthreads();
       PROF(4);
       gram_rows_acc<Q>(gh, gl, ei, ej, Tb, d1, jn * q3);
