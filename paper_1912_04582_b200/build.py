@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libttdvm_cuda.so")
-SOURCES = ["round.cu", "physics.cu", "facefactor.cu", "capi.cu"]
+SOURCES = ["round.cu", "round256.cu", "physics.cu", "facefactor.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr"]
@@ -32,9 +32,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for s in SOURCES:  # the translation units compile in parallel
         o = os.path.join(CSRC, s.replace(".cu", ".o"))
         objs.append(o)
+        deps = [os.path.join(CSRC, s), *headers]
+        if s == "round256.cu":  # includes round.cu
+            deps.append(os.path.join(CSRC, "round.cu"))
         if not force and os.path.exists(o) and all(
-                os.path.getmtime(d) <= os.path.getmtime(o)
-                for d in [os.path.join(CSRC, s), *headers] if os.path.exists(d)):
+                os.path.getmtime(d) <= os.path.getmtime(o) for d in deps if os.path.exists(d)):
             continue  # object newer than its source and every header
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:

@@ -26,12 +26,24 @@
 
 namespace ttdvm {
 cudaError_t launch_round(const RoundArgs& a, cudaStream_t st);
-cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_round_bins(const RoundArgs& a, int* counts, int* bmax, int* lists,
                               cudaStream_t st);
-size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX, int JB, bool spill);
-long long round_gram_spill_doubles(int n1, int n3, int RM1, int RM2);
-cudaError_t round_gram_resident(const RoundArgs& a, int* resident);
+// exact-Gram rounding kernels, 128-thread (round.cu) and 256-thread
+// (round256.cu) CTAs; same source, same plan
+#define TTDVM_GRAM_API                                                                        \
+  size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX, int JB, bool spill); \
+  long long round_gram_spill_doubles(int n1, int n3, int RM1, int RM2);                        \
+  cudaError_t round_gram_resident(const RoundArgs& a, int* resident);                          \
+  cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st);
+namespace g128 {
+TTDVM_GRAM_API
+}
+namespace g256 {
+TTDVM_GRAM_API
+}
+#undef TTDVM_GRAM_API
+using g128::round_gram_smem_bytes;  // the plan does not depend on the CTA width
+using g128::round_gram_spill_doubles;
 size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int MSMAX);
 struct MacroArgs {
   TSet set;
@@ -416,13 +428,22 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   constexpr size_t kSmemMax = 227 * 1024;
   struct Launch {
     int bin, count, rm1, rm2, ms, jb;
-    bool spill;
+    bool spill, wide;
   };
-  // CTAs per SM the kernel variant is built for (launch bounds by Gram size)
+  // 256-thread CTAs from Gram dimension TTDVM_WIDE_D (default 16) up: the
+  // measured crossover between the short-phase small tiles (128 threads, four
+  // CTAs per SM) and the slice-product-heavy larger ones
+  static const int wide_d = [] {
+    const char* e = getenv("TTDVM_WIDE_D");
+    return e ? atoi(e) : 16;
+  }();
+  auto gram_d = [&](int rm1, int rm2) { return std::max(std::min(n, rm1), std::min(n, rm2)); };
+  // CTAs per SM the kernel variant is built for (its launch bounds)
   auto blocks_per_sm = [&](int rm1, int rm2) {
-    const int d = std::max(std::min(n, rm1), std::min(n, rm2));
+    const int d = gram_d(rm1, rm2);
     const int ne = d * (d + 1) / 2;
-    return ne <= 3 * kRoundThreads ? 4 : (ne <= 10 * kRoundThreads ? 3 : 1);
+    if (d >= wide_d) return ne <= 3 * 256 ? 2 : 1;
+    return ne <= 3 * 128 ? 4 : (ne <= 10 * 128 ? 3 : 1);
   };
   // slices per barrier phase: about a quarter of the slices (measured best
   // on config 4: fewer phases pay for a lower CTA count), shrunk while the
@@ -439,7 +460,9 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   for (int b = kRankBins - 1; b >= 0; --b) {  // large ranks first (long CTAs start early)
     if (!bcount[b]) continue;
     const int* bm = bmax + kBinWords * b;
-    Launch l{b, bcount[b], std::max(1, bm[0]), std::max(1, bm[1]), std::max(1, bm[2]), 1, false};
+    Launch l{b, bcount[b], std::max(1, bm[0]), std::max(1, bm[1]), std::max(1, bm[2]), 1, false,
+             false};
+    l.wide = gram_d(l.rm1, l.rm2) >= wide_d;
     // working sets above the shared-memory budget (n = 64, summed ranks of
     // ~100 and more) take the spill plan: F, last^T, XP and the Gram region
     // in a per-CTA global scratch slice, persistent CTAs
@@ -507,14 +530,16 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
         int grid = l.count;
         if (l.spill) {
           int resident = 0;
-          CK(round_gram_resident(a, &resident));
+          CK(l.wide ? g256::round_gram_resident(a, &resident)
+                    : g128::round_gram_resident(a, &resident));
           if (resident <= 0) throw Fail{TTDVM_ENOMEM, "spill rounding plan does not fit an SM"};
           grid = std::min(l.count, resident);
           a.gstride = round_gram_spill_doubles(n, n, l.rm1, l.rm2);
           c->d_gscratch.alloc((size_t)grid * (size_t)a.gstride);
           a.gscratch = c->d_gscratch.p;
         }
-        CK(launch_round_gram(a, grid, c->st));
+        CK(l.wide ? g256::launch_round_gram(a, grid, c->st)
+                  : g128::launch_round_gram(a, grid, c->st));
         c->launches += 1;
       }
     }

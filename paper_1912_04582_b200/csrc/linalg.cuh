@@ -11,7 +11,13 @@
 namespace ttdvm {
 namespace {
 
-constexpr int NT = kRoundThreads;
+// A translation unit may build the helpers for another CTA width
+// (round256.cu sets 256 for the wide rounding kernel).
+#ifndef TTDVM_ROUND_NT
+#define TTDVM_ROUND_NT 128
+#endif
+static_assert(TTDVM_ROUND_NT == kRoundThreads || TTDVM_ROUND_NT == 256, "CTA width");
+constexpr int NT = TTDVM_ROUND_NT;
 constexpr int NW = NT / 32;
 
 __device__ __forceinline__ double warp_sum(double v) {

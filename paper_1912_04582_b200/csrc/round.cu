@@ -769,6 +769,7 @@ __device__ __forceinline__ void gram_store(double* Gh, double* Gl, int d, double
 
 }  // namespace
 
+#ifndef TTDVM_GRAM_ONLY
 template <bool SMALL>
 __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs p) {
   extern __shared__ double sm[];
@@ -1034,6 +1035,8 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
 #undef PROF
 }
 
+#endif  // TTDVM_GRAM_ONLY
+
 // ---------------------------------------------------------------------------
 // Exact-Gram route (default): the two tall QRs of the TSQR route are
 // replaced by Gram matrices accumulated in double-double (every product
@@ -1043,6 +1046,19 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
 // as the Householder R (rounding R to FP64) -- the rank decisions keep the
 // accuracy of the QR route -- while the slice loop has no sequential
 // column steps (3 barriers per slice instead of 2 per column).
+// The exact-Gram kernel and its launchers are compiled for two CTA widths:
+// 128 threads here (namespace g128) and 256 threads in round256.cu
+// (namespace g256, TTDVM_GRAM_ONLY).  Measured: the small Gram tiles of the
+// config-4 face fluxes run best on 128 threads (their phases are short and
+// four CTAs share an SM), the larger ones (cell residuals, config 3,
+// n = 64) on 256 (more threads per dense slice product).
+#if TTDVM_ROUND_NT == 256
+#define RG_NS g256
+#else
+#define RG_NS g128
+#endif
+namespace RG_NS {
+
 // Buffer plan of the exact-Gram kernel (doubles).  Shared: everything;
 // with `spill`, F, last^T, XP and the Gram region move to a per-CTA global
 // scratch slice (gdoubles) and JB must be 1.
@@ -1465,7 +1481,7 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
 // Shared-memory plans: one CTA per output (6 / 4 / 3 CTAs per SM by Gram
 // size); SPILL launches are persistent (grid = resident CTAs) and loop.
 template <int Q, bool SPILL>
-__global__ void __launch_bounds__(NT, SPILL ? 1 : (Q <= 3 ? 4 : (Q <= 10 ? 3 : 1)))
+__global__ void __launch_bounds__(NT, SPILL ? 1 : (Q <= 3 ? 512 / NT : (Q <= 10 ? (NT == 128 ? 3 : 1) : 1)))
     round_gram_kernel(RoundArgs p) {
   extern __shared__ double sm[];
   __shared__ int s_meta[8];
@@ -1533,6 +1549,8 @@ static cudaError_t launch_gram_q(const RoundArgs& a, int grid, size_t smem, cuda
     LAUNCH_Q(10)
   } else if (ne <= 17 * NT) {
     LAUNCH_Q(17)
+  } else if (NT < 256 && ne <= 33 * NT) {
+    LAUNCH_Q(33)
   } else {
     return cudaErrorInvalidValue;
   }
@@ -1557,6 +1575,9 @@ cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st) 
   return launch_gram_q<false>(a, nblocks, smem, st, nullptr);
 }
 
+}  // namespace RG_NS
+
+#ifndef TTDVM_GRAM_ONLY
 // Shared-memory bytes of the plan above.
 size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int MSMAX) {
   (void)n2;
@@ -1629,5 +1650,7 @@ cudaError_t launch_round(const RoundArgs& a, cudaStream_t st) {
     round_sums_kernel<false><<<a.nout, NT, smem, st>>>(a);
   return cudaGetLastError();
 }
+
+#endif  // TTDVM_GRAM_ONLY
 
 }  // namespace ttdvm
