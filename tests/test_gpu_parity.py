@@ -363,3 +363,27 @@ def test_partitioned_step_two_contexts():
             g = int(part.owned[lc])
             assert rel_err(st.full(lc), f[g].to_full()) <= 10 * p.eps
         c.close()
+
+
+def test_config2_full_size_conservation(ctx):
+    """Config 2 at its full size (32^3 periodic cells, 24^3 velocity mesh):
+    size-independent properties of the step -- interior fluxes telescope
+    and the S-model collision conserves mass and momentum, so the totals
+    sum_i n_i V_i and sum_i n_i u_i V_i stay put to the rounding budget
+    (SPEC.md:415); states stay finite with ranks <= n."""
+    p = config(2)
+    assert p.mesh.ncell == 32768
+    ctx.setup(p)
+    vol = p.mesh.cell_volume
+    ctx.step(p.dt, p.eps, p.cap, 1)
+    m0 = ctx.macros()  # macroparameters of t^0
+    k = 8
+    ctx.step(p.dt, p.eps, p.cap, k)
+    mk = ctx.macros()  # of t^k
+    mass0, massk = np.sum(m0[:, 0] * vol), np.sum(mk[:, 0] * vol)
+    assert abs(massk - mass0) <= 10 * p.eps * k * mass0
+    mom0 = (m0[:, 0] * vol) @ m0[:, 1:4]
+    momk = (mk[:, 0] * vol) @ mk[:, 1:4]
+    assert np.all(np.abs(momk - mom0) <= 10 * p.eps * k * mass0)
+    st = ctx.download_state()
+    assert np.all(np.isfinite(st.cores)) and st.ranks.max() <= p.nv
