@@ -331,11 +331,18 @@ def run_config3(args):
         ms = float(t.item())
     value = world * count * args.steps / (ms / 1e3)
     ctx.set_profiling(False)
-    # e2e: host summands -> device, round, result -> host, every step
+    # e2e: host summands -> device, round, result -> host, every step, from /
+    # into pinned host buffers (filled before the timed region)
+    from paper_1912_04582_b200.tt_batch import TtBatch
+    pin_in = torch.empty(b.cores.size, dtype=torch.float64, pin_memory=True).numpy()
+    pin_in[:] = b.cores
+    b = TtBatch(b.n1, b.n2, b.n3, b.ranks, b.offsets, pin_in)
+    pin_out = torch.empty(count * (32 * 32 * 34), dtype=torch.float64,  # max ranks (32, 32)
+                          pin_memory=True).numpy()
     t0 = time.perf_counter()
     d2h = 0
     for _ in range(args.e2e_steps):
-        out = ctx.rounded(b, eps, 0, group_off=go)
+        out = ctx.rounded(b, eps, 0, group_off=go, out=pin_out)
         d2h += int(out.cores.nbytes + out.ranks.nbytes + out.offsets.nbytes)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -492,7 +499,14 @@ def main():
     # download state -- every step
     ctx.set_profiling(False)
     # (the host state advances: steps 1..E from the initial state, as timed)
-    host = f_local
+    # pinned host buffer for the state's cores (the ranks / offsets arrays
+    # are small); the initial state is copied in before the timed region
+    from paper_1912_04582_b200.tt_batch import TtBatch
+    pinned = torch.empty(max(2 * f_local.cores.size, 1 << 20), dtype=torch.float64,
+                         pin_memory=True).numpy()
+    pinned[:f_local.cores.size] = f_local.cores
+    host = TtBatch(f_local.n1, f_local.n2, f_local.n3, f_local.ranks, f_local.offsets,
+                   pinned[:f_local.cores.size])
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
@@ -503,7 +517,7 @@ def main():
         ctx.step(p.dt, p.eps, p.cap, 1)
         if part is not None:
             halo.exchange(part, pack, unpack, p.nv, device=torch.device("cuda", local))
-        host = ctx.download_state()
+        host = ctx.download_state(out=pinned)
         d2h += int(host.cores.nbytes + host.ranks.nbytes + host.offsets.nbytes)
     h2d //= args.e2e_steps
     d2h //= args.e2e_steps

@@ -45,6 +45,14 @@ struct TermInfo {
   int b1, b2, fa1, fa2;
 };
 
+// x / d for 0 <= x < 2^20 and 1 <= d <= 2^10 through the FP32 reciprocal
+// inv = rn(1/d): (x + 0.5) inv is (x + 0.5) / d within 2^-23 relative, and
+// that quotient is at least 0.5 / d (>= 2^-21 relative) from the nearest
+// integer, so truncation is exact.
+__device__ __forceinline__ int small_div(int x, float inv) {
+  return __float2int_rz(((float)x + 0.5f) * inv);
+}
+
 // prefetch.global.L1 of the 128-byte lines covering [p, p + count)
 __device__ __forceinline__ void prefetch_l1(const double* p, long long count) {
   const unsigned long long a0 = reinterpret_cast<unsigned long long>(p) & ~127ull;
@@ -633,13 +641,14 @@ __device__ void stage_slices(double* Ms, int msld, const TermInfo* terms, int K,
     const double* mf = t.fb ? t.fb + (long long)n1 * fa1 : nullptr;
     const double* u1 = t.u[1];
     const bool rev = t.refl == 2;
+    const float ir1 = __frcp_rn((float)r1), ib1 = __frcp_rn((float)b1), ib2 = __frcp_rn((float)b2);
     double* dst = Ms + t.ms;
     for (int r = threadIdx.x & ((1 << lg) - 1); r < sz; r += 1 << lg) {
       int os = r, of = 0;
       if (mf) {  // Kronecker block A2_j (x) B2_j: (p*b1 + q, p'*b2 + q') = A(p,p') B(q,q')
-        const int c = r / r1, a = r - c * r1;
-        const int pa = a / b1, q = a - pa * b1;
-        const int pc = c / b2, qq = c - pc * b2;
+        const int c = small_div(r, ir1), a = r - c * r1;
+        const int pa = small_div(a, ib1), q = a - pa * b1;
+        const int pc = small_div(c, ib2), qq = c - pc * b2;
         os = q + b1 * qq;
         of = pa + fa1 * pc;
       }
@@ -1598,32 +1607,59 @@ size_t round_smem_bytes(int n1, int n2, int n3, int RM1, int RM2, int HMAX, int 
 // outputs with kRankEdges[b-1] < key <= kRankEdges[b]; bmax[4 b + {0,1,2}]
 // are the bin's RM1, RM2, MSMAX.  Order inside a bin is nondeterministic;
 // every output is computed independently, so results are not.
-__global__ void round_bin_kernel(RoundArgs p, int* counts, int* bmax, int* lists) {
-  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < p.nout; o += gridDim.x * blockDim.x) {
-    const long long t0 = p.term_off ? p.term_off[o] : o;
-    const int K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
-    int r1 = 0, r2 = 0, ms = 0;
-    for (int k = 0; k < K; ++k) {
-      const Term tm = p.terms[t0 + k];
-      const TSet& s = p.sets[tm.set];
-      int a = s.ranks[2 * tm.idx], b = s.ranks[2 * tm.idx + 1];
-      if (tm.fset >= 0) {
-        a *= p.sets[tm.fset].ranks[2 * tm.fidx];
-        b *= p.sets[tm.fset].ranks[2 * tm.fidx + 1];
-      }
-      r1 += a;
-      r2 += b;
-      ms += a * b;
+__global__ void __launch_bounds__(256) round_bin_kernel(RoundArgs p, int* counts, int* bmax,
+                                                        int* lists) {
+  // Block-aggregated: per-bin counts and maxima are reduced in shared memory
+  // and each block reserves one range per bin with a single global atomic
+  // (the per-output global atomics of a 1.5 M-output launch contended on 44
+  // addresses).
+  __shared__ int s_cnt[kRankBins], s_base[kRankBins], s_max[kRankBins * kBinWords];
+  for (int o0 = blockIdx.x * blockDim.x; o0 < p.nout; o0 += gridDim.x * blockDim.x) {
+    for (int i = threadIdx.x; i < kRankBins * (1 + kBinWords); i += blockDim.x) {
+      if (i < kRankBins) s_cnt[i] = 0;
+      else s_max[i - kRankBins] = 0;
     }
-    const int key = max(r1, r2);
-    int bin = 0;
-    while (bin < kRankBins - 1 && key > kRankEdges[bin]) ++bin;
-    const int pos = atomicAdd(&counts[bin], 1);
-    lists[(long long)bin * p.nout + pos] = o;
-    atomicMax(&bmax[kBinWords * bin], r1);
-    atomicMax(&bmax[kBinWords * bin + 1], r2);
-    atomicMax(&bmax[kBinWords * bin + 2], ms);
-    atomicMax(&bmax[kBinWords * bin + 3], K);
+    __syncthreads();
+    const int o = o0 + threadIdx.x;
+    int bin = -1, pos = 0;
+    if (o < p.nout) {
+      const long long t0 = p.term_off ? p.term_off[o] : o;
+      const int K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
+      int r1 = 0, r2 = 0, ms = 0;
+      for (int k = 0; k < K; ++k) {
+        const Term tm = p.terms[t0 + k];
+        const TSet& s = p.sets[tm.set];
+        int a = s.ranks[2 * tm.idx], b = s.ranks[2 * tm.idx + 1];
+        if (tm.fset >= 0) {
+          a *= p.sets[tm.fset].ranks[2 * tm.fidx];
+          b *= p.sets[tm.fset].ranks[2 * tm.fidx + 1];
+        }
+        r1 += a;
+        r2 += b;
+        ms += a * b;
+      }
+      const int key = max(r1, r2);
+      bin = 0;
+      while (bin < kRankBins - 1 && key > kRankEdges[bin]) ++bin;
+      pos = atomicAdd(&s_cnt[bin], 1);
+      atomicMax(&s_max[kBinWords * bin], r1);
+      atomicMax(&s_max[kBinWords * bin + 1], r2);
+      atomicMax(&s_max[kBinWords * bin + 2], ms);
+      atomicMax(&s_max[kBinWords * bin + 3], K);
+    }
+    __syncthreads();
+    if (threadIdx.x < kRankBins) {
+      const int b = threadIdx.x;
+      if (s_cnt[b] > 0) {
+        s_base[b] = atomicAdd(&counts[b], s_cnt[b]);
+        for (int w = 0; w < kBinWords; ++w)
+          if (s_max[kBinWords * b + w] > bmax[kBinWords * b + w])
+            atomicMax(&bmax[kBinWords * b + w], s_max[kBinWords * b + w]);
+      }
+    }
+    __syncthreads();
+    if (bin >= 0) lists[(long long)bin * p.nout + s_base[bin] + pos] = o;
+    __syncthreads();
   }
 }
 

@@ -195,19 +195,25 @@ class Context:
         s = _batch_struct(b)
         self._check(self.lib.ttdvm_cuda_upload_state(self.h, C.byref(s)))
 
-    def _fetch(self, count, layout_fn, download_fn) -> TtBatch:
+    def _fetch(self, count, layout_fn, download_fn, out=None) -> TtBatch:
         ranks = np.zeros(2 * max(count, 1), dtype=np.int32)
         offs = np.zeros(count + 1, dtype=np.int64)
         self._check(layout_fn(_ptr(ranks), _ptr(offs)))
-        cores = np.zeros(max(1, int(offs[count])), dtype=np.float64)
+        need = max(1, int(offs[count]))
+        if out is not None and out.dtype == np.float64 and out.size >= need:
+            cores = out  # caller-owned (e.g. pinned) buffer, written in place
+        else:
+            cores = np.empty(need, dtype=np.float64)
         self._check(download_fn(_ptr(cores), int(cores.size)))
         return TtBatch(self.n, self.n, self.n, ranks[:2 * count], offs, cores[:int(offs[count])])
 
-    def download_state(self) -> TtBatch:
+    def download_state(self, out=None) -> TtBatch:
+        """The state in cell order.  ``out``: optional float64 buffer (e.g.
+        pinned host memory) the cores are written into when large enough."""
         count = self.mesh.ncell
         return self._fetch(count,
                            lambda r, o: self.lib.ttdvm_cuda_state_layout(self.h, r, o),
-                           lambda c, cap: self.lib.ttdvm_cuda_download_state(self.h, c, cap))
+                           lambda c, cap: self.lib.ttdvm_cuda_download_state(self.h, c, cap), out)
 
     def stage(self, name: str) -> TtBatch:
         sid = STAGE[name]
@@ -263,8 +269,9 @@ class Context:
         return out
 
     def rounded(self, b: TtBatch, eps: float, cap: int = 0, group_off=None, scale=None,
-                margins: bool = False):
-        """Batched TtTensor::rounded of (optionally grouped, scaled) sums."""
+                margins: bool = False, out=None):
+        """Batched TtTensor::rounded of (optionally grouped, scaled) sums.
+        ``out``: optional float64 (e.g. pinned) buffer for the result cores."""
         s = _batch_struct(b)
         nout = b.count if group_off is None else len(group_off) - 1
         go = None if group_off is None else np.ascontiguousarray(group_off, dtype=np.int64)
@@ -274,7 +281,7 @@ class Context:
                                                     float(eps), int(cap), _ptr(mg)))
         self._last_nout = nout
         out = self._fetch(nout, lambda r, o: self.lib.ttdvm_cuda_result_layout(self.h, r, o),
-                          lambda c, cap_: self.lib.ttdvm_cuda_result_download(self.h, c, cap_))
+                          lambda c, cap_: self.lib.ttdvm_cuda_result_download(self.h, c, cap_), out)
         if margins:
             return out, mg[:2 * nout].reshape(nout, 2)
         return out

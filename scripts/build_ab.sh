@@ -5,7 +5,7 @@ REV=$1; NAME=$2
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 TMP=$(mktemp -d)
 git -C "$ROOT" archive "$REV" paper_1912_04582_b200/csrc include | tar -x -C "$TMP"
-mkdir -p "$ROOT/build_ab"
+mkdir -p "$ROOT/build_ab"  # NB: listed in .gpurunignore; copy the .so under paper_1912_04582_b200/ab/ to ship it
 OBJS=""
 for f in "$TMP"/paper_1912_04582_b200/csrc/*.cu; do
   o="${f%.cu}.o"
