@@ -34,6 +34,7 @@ cudaError_t launch_round_bins(const RoundArgs& a, int* counts, int* bmax, int* l
   size_t round_gram_smem_bytes(int n1, int n3, int RM1, int RM2, int MSMAX, int JB, bool spill); \
   long long round_gram_spill_doubles(int n1, int n3, int RM1, int RM2);                        \
   cudaError_t round_gram_resident(const RoundArgs& a, int* resident);                          \
+  int round_gram_tiny_d();                                                                     \
   cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st);
 namespace g128 {
 TTDVM_GRAM_API
@@ -443,6 +444,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     const int d = gram_d(rm1, rm2);
     const int ne = d * (d + 1) / 2;
     if (d >= wide_d) return ne <= 3 * 256 ? 2 : 1;
+    if (d <= g128::round_gram_tiny_d()) return 8;  // the tiny variant's launch bounds
     return ne <= 3 * 128 ? 4 : (ne <= 10 * 128 ? 3 : 1);
   };
   // slices per barrier phase: about a quarter of the slices (measured best

@@ -28,6 +28,7 @@
 // reference's up to roundoff; cores differ by an orthogonal gauge (the
 // reference keeps Sigma_2 in last, here it sits in middle).
 #include <math.h>
+#include <stdlib.h>
 
 #include "linalg.cuh"
 
@@ -1489,19 +1490,23 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
 
 // Shared-memory plans: one CTA per output (6 / 4 / 3 CTAs per SM by Gram
 // size); SPILL launches are persistent (grid = resident CTAs) and loop.
+// Q = 0 is the Q = 1 body built for 1024 / NT resident CTAs (64 registers at
+// 128 threads): tiny Gram tiles (D <= kTinyD), whose plans fit eight CTAs
+// per SM in shared memory.
 template <int Q, bool SPILL>
-__global__ void __launch_bounds__(NT, SPILL ? 1 : (Q <= 3 ? 512 / NT : (Q <= 10 ? (NT == 128 ? 3 : 1) : 1)))
+__global__ void __launch_bounds__(NT, SPILL ? 1 : (Q == 0 ? 1024 / NT : (Q <= 3 ? 512 / NT : (Q <= 10 ? (NT == 128 ? 3 : 1) : 1))))
     round_gram_kernel(RoundArgs p) {
+  constexpr int QB = Q == 0 ? 1 : Q;
   extern __shared__ double sm[];
   __shared__ int s_meta[8];
   if constexpr (!SPILL) {
     const int o = p.olist ? p.olist[blockIdx.x] : blockIdx.x;
-    if (o < p.nout) round_gram_body<Q, false>(p, o, sm, s_meta);
+    if (o < p.nout) round_gram_body<QB, false>(p, o, sm, s_meta);
   } else {
     for (int b = blockIdx.x; b < p.nblk; b += gridDim.x) {
       const int o = p.olist ? p.olist[b] : b;
       __syncthreads();  // the previous output's shared-memory readers are done
-      if (o < p.nout) round_gram_body<Q, true>(p, o, sm, s_meta);
+      if (o < p.nout) round_gram_body<QB, true>(p, o, sm, s_meta);
     }
   }
 }
@@ -1523,6 +1528,19 @@ long long round_gram_spill_doubles(int n1, int n3, int RM1, int RM2) {
   const GramPlan g = gram_plan(n1, n3, RM1, RM2, 1);
   const long long d = 2LL * n1 * g.RMX + (long long)n3 * RM2 + g.GZ;
   return (d + 31) / 32 * 32;
+}
+
+// Largest Gram dimension D that takes the 8-CTA tiny variant (128-thread
+// build): TTDVM_TINY_D, default 0 = off.  Measured on config 4 (half scale,
+// same box): D <= 8 cuts the collision roundings by ~24 % but slows the
+// update roundings about as much (spills at 64 registers); D <= 12 doubles
+// the flux phase.
+int round_gram_tiny_d() {
+  static const int v = [] {
+    const char* e = getenv("TTDVM_TINY_D");
+    return e ? atoi(e) : 0;
+  }();
+  return NT == 128 ? v : 0;
 }
 
 template <bool SPILL>
@@ -1548,7 +1566,15 @@ static cudaError_t launch_gram_q(const RoundArgs& a, int grid, size_t smem, cuda
     }                                                                                        \
     kern<<<grid, NT, smem, st>>>(a);                                                         \
   }
-  if (ne <= NT) {
+  bool tiny = false;
+  if constexpr (!SPILL && NT == 128) {
+    if (D <= round_gram_tiny_d()) {
+      tiny = true;
+      LAUNCH_Q(0)
+    }
+  }
+  if (tiny) {
+  } else if (ne <= NT) {
     LAUNCH_Q(1)
   } else if (ne <= 3 * NT) {
     LAUNCH_Q(3)
