@@ -35,6 +35,7 @@ cudaError_t launch_round_bins(const RoundArgs& a, int* counts, int* bmax, int* l
   long long round_gram_spill_doubles(int n1, int n3, int RM1, int RM2);                        \
   cudaError_t round_gram_resident(const RoundArgs& a, int* resident);                          \
   int round_gram_tiny_d();                                                                     \
+  int round_gram_tiny_minb();                                                                  \
   cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st);
 namespace g128 {
 TTDVM_GRAM_API
@@ -444,7 +445,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     const int d = gram_d(rm1, rm2);
     const int ne = d * (d + 1) / 2;
     if (d >= wide_d) return ne <= 3 * 256 ? 2 : 1;
-    if (d <= g128::round_gram_tiny_d()) return 8;  // the tiny variant's launch bounds
+    if (d <= g128::round_gram_tiny_d()) return g128::round_gram_tiny_minb();  // its launch bounds
     return ne <= 3 * 128 ? 4 : (ne <= 10 * 128 ? 3 : 1);
   };
   // slices per barrier phase: about a quarter of the slices (measured best
@@ -1386,9 +1387,14 @@ int ttdvm_cuda_round_batch(ttdvm_ctx* c, const ttdvm_tt_batch* in, int32_t nout,
     cudaSetDevice(c->device);
     upload_batch(c, in, c->in);
     TermList& tl = c->t_batch;
+    require(nout >= 0, "rounded: negative output count");
     tl.off.resize(nout + 1);
     tl.terms.clear();
-    for (int o = 0; o <= nout; ++o) tl.off[o] = group_off ? group_off[o] : o;
+    for (int o = 0; o <= nout; ++o) {
+      tl.off[o] = group_off ? group_off[o] : o;
+      require(o == 0 ? tl.off[0] == 0 : tl.off[o] > tl.off[o - 1],
+              "group offsets must start at 0 and increase (every sum has a summand)");
+    }
     require(tl.off[nout] == in->count, "group offsets must cover the input batch");
     for (int t = 0; t < in->count; ++t)
       tl.terms.push_back(Term{S_IN, t, scale ? scale[t] : 1.0, -1, 0});

@@ -1493,8 +1493,11 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
 // Q = 0 is the Q = 1 body built for 1024 / NT resident CTAs (64 registers at
 // 128 threads): tiny Gram tiles (D <= kTinyD), whose plans fit eight CTAs
 // per SM in shared memory.
+#ifndef TTDVM_TINY_MINB
+#define TTDVM_TINY_MINB 8
+#endif
 template <int Q, bool SPILL>
-__global__ void __launch_bounds__(NT, SPILL ? 1 : (Q == 0 ? 1024 / NT : (Q <= 3 ? 512 / NT : (Q <= 10 ? (NT == 128 ? 3 : 1) : 1))))
+__global__ void __launch_bounds__(NT, SPILL ? 1 : (Q == 0 ? TTDVM_TINY_MINB * 128 / NT : (Q <= 3 ? 512 / NT : (Q <= 10 ? (NT == 128 ? 3 : 1) : 1))))
     round_gram_kernel(RoundArgs p) {
   constexpr int QB = Q == 0 ? 1 : Q;
   extern __shared__ double sm[];
@@ -1542,6 +1545,7 @@ int round_gram_tiny_d() {
   }();
   return NT == 128 ? v : 0;
 }
+int round_gram_tiny_minb() { return TTDVM_TINY_MINB; }
 
 template <bool SPILL>
 static cudaError_t launch_gram_q(const RoundArgs& a, int grid, size_t smem, cudaStream_t st,

@@ -387,3 +387,40 @@ def test_config2_full_size_conservation(ctx):
     assert np.all(np.abs(momk - mom0) <= 10 * p.eps * k * mass0)
     st = ctx.download_state()
     assert np.all(np.isfinite(st.cores)) and st.ranks.max() <= p.nv
+
+
+def test_round_batch_edge_inputs(ctx):
+    """Empty and ragged batches, bad arguments and non-finite data through
+    the C ABI (the reference throws std::invalid_argument for argument and
+    shape errors, proj/src/tt_tensor.cpp:139-145; a non-finite sum has no
+    rounding)."""
+    rng = np.random.default_rng(41)
+    n = 10
+    ctx.set_grid(n, 1.0)
+    empty = TtBatch.from_list([], n=n)
+    got = ctx.rounded(empty, 1e-8, group_off=[0])
+    assert got.count == 0
+    # ragged: every tensor its own ranks, groups of 1..4 summands
+    ts = [random_tt(rng, n, n, n, int(rng.integers(1, 7)), int(rng.integers(1, 7)))
+          for _ in range(10)]
+    groups = [[(ts[0], 1.0)], [(ts[1], 1.0), (ts[2], -2.0)],
+              [(ts[3], 1.0), (ts[4], 0.5), (ts[5], 1.0), (ts[6], 3.0)],
+              [(ts[7], 1.0), (ts[8], 1.0), (ts[9], -1.0)]]
+    check_round(ctx, groups, 1e-9)
+    with pytest.raises(ValueError):
+        ctx.rounded(TtBatch.from_list(ts[:2]), 0.0)  # eps must be > 0
+    bad = TtBatch.from_list(ts[:2])
+    bad.offsets[1] += 1
+    with pytest.raises(ValueError):
+        ctx.rounded(bad, 1e-8)  # offsets inconsistent with the ranks
+    with pytest.raises(ValueError):
+        ctx.rounded(TtBatch.from_list(ts[:2]), 1e-8, group_off=[0, 3])  # groups past the batch
+    nanb = TtBatch.from_list(ts[:1])
+    nanb.cores[5] = np.nan
+    with pytest.raises(RuntimeError):
+        ctx.rounded(nanb, 1e-8)
+    # the context stays usable after the errors
+    got = ctx.rounded(TtBatch.from_list(ts[:1]), 1e-12)
+    assert rel_err(got.full(0), ts[0].to_full()) < 1e-11
+    with pytest.raises(ValueError):
+        ctx.rounded(TtBatch.from_list(ts[:2]), 1e-8, group_off=[0, 0, 2])  # an empty sum
