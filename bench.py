@@ -546,7 +546,12 @@ def main():
     dom = int(np.argmax(phase_ms[2:7])) + 2
     dom_s = phase_ms[dom] / 1e3
     achieved = flops[dom] / dom_s / 1e12 if dom_s > 0 else 0.0
-    traffic = traffic_from_profiles().get(names[dom])
+    # ncu DRAM bytes per rounded output of this phase (profiles/traffic.json),
+    # times the phase's outputs per launch in this run
+    per_out = traffic_from_profiles().get(names[dom] + "_bytes_per_output")
+    nface_local = (part.mesh if part is not None else p.mesh).nface
+    outs_per_step = {"round_flux": nface_local}.get(names[dom], cells_per_rank)
+    traffic = (per_out * outs_per_step * args.steps / max(1, launches[dom]) if per_out else None)
     roofline = {"bound": "fp64", "kernel": f"round_gram_kernel ({names[dom]})",
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak if fp64_peak else None,
