@@ -498,6 +498,7 @@ def main():
     phase_ms = ctx.phase_times()
     flops, bytes_, launches = ctx.phase_work()
     gpu_launches = ctx.launch_count()
+    setup["cell_blocks"] = ctx.setup_info()["cell_blocks"]  # grown on out-of-memory
     st = ctx.download_state()
     max_rank = int(st.ranks.max())
     if dist:

@@ -95,6 +95,15 @@ int ttdvm_cuda_download_state(ttdvm_ctx* ctx, double* cores, int64_t capacity);
  * the reference). */
 int ttdvm_cuda_step(ttdvm_ctx* ctx, double dt, double eps, int32_t cap, int32_t nsteps);
 
+/* Bounded-memory step: the face fluxes, residuals and updates of a step are
+ * formed in `nblocks` contiguous ranges of the owned cells (the fluxes of
+ * faces between two blocks are rounded in both), so the flux and residual
+ * arenas hold one block at a time.  Same sums, same results as one block.
+ * nblocks = 0 (default): one block, multiplied by 4 whenever a step runs out
+ * of device memory.  No reference counterpart (the reference holds every
+ * intermediate in host memory). */
+int ttdvm_cuda_set_blocks(ttdvm_ctx* ctx, int32_t nblocks);
+
 /* Multi-GPU slab partition: cells [0, nowned) of the
  * mesh are stepped, the rest are halo ghosts whose states the caller
  * refreshes after every step with the two calls below (packed in the
@@ -167,8 +176,9 @@ int ttdvm_cuda_wall_densities(ttdvm_ctx* ctx, double* out);
 
 /* Set-up facts of the last step's mesh: [0] distinct oblique normals,
  * [1] of them with a kept singular value below 1e-14 sigma_max (the FP64
- * operand's own noise), [2] wall faces, [3] face-factor build time (us). */
-int ttdvm_cuda_setup_info(ttdvm_ctx* ctx, int64_t* info4);
+ * operand's own noise), [2] wall faces, [3] face-factor build time (us),
+ * [4] cell blocks of the step (ttdvm_cuda_set_blocks). */
+int ttdvm_cuda_setup_info(ttdvm_ctx* ctx, int64_t* info5);
 
 /* Device time (ms) of the kernels of the last call, by phase:
  * [0] moments, [1] shakhov build, [2] round f_S, [3] round collision,

@@ -242,6 +242,14 @@ struct ttdvm_ctx {
   std::vector<double> factors;
   DevBuf<double> d_factors;
   TermList t_fs, t_col, t_flux, t_res, t_upd, t_batch;
+  // blocked step (bounded memory): owned cells in nblocks contiguous ranges,
+  // each with its own flux (faces it touches), residual and update lists
+  int nblocks = 1;           // blocks in use
+  bool auto_blocks = true;   // grow nblocks when the step runs out of memory
+  int built_blocks = 0;      // nblocks the per-block lists were built for
+  std::vector<int> blk_c0;   // [nblocks + 1] cell ranges
+  std::vector<TermList> bt_flux, bt_res, bt_upd;
+  unsigned long long h_base_used = 0;
   // tensor sets
   TensorSet state[2];
   int cur = 0;
@@ -370,10 +378,16 @@ void ensure_static(ttdvm_ctx* c) {
 
 // Run one rounding launch: sets bound into RoundArgs, output into `out`.
 // Repeats the launch with a larger arena if it overflowed.
+void grow_preserve(ttdvm_ctx* c, TensorSet& s, long long keep, long long need);
+
+// Round the sums of `tl` into `out`.  obase >= 0 selects append mode (the
+// blocked step): output o becomes entry obase + o of `out` (sized by the
+// caller) and is placed after the `out.used` doubles already in its arena.
 void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets], TensorSet& out,
-               double eps, int cap, double* margins_dev) {
+               double eps, int cap, double* margins_dev, long long obase = -1) {
   const int nout = tl.nout();
-  out.resize(nout);
+  const bool append = obase >= 0;
+  if (!append) out.resize(nout);
   if (nout == 0) return;
   require(tl.maxk <= kMaxTerms, "too many summands per rounded output");
   ensure_static(c);
@@ -491,7 +505,11 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   a.HMAX = HMAX;
   // arena: a modest first estimate; an overflowing launch reports the exact
   // total (the bump counter keeps counting), so one retry always suffices
-  if (out.arena.n == 0) {
+  const long long base_used = append ? out.used : 0;
+  if (append) {
+    const int re = std::min(n, 4);
+    grow_preserve(c, out, base_used, base_used + (long long)nout * tt_size(n, n, n, re, re) + 1024);
+  } else if (out.arena.n == 0) {
     const int re = std::min(n, 4);
     out.arena.alloc((size_t)nout * tt_size(n, n, n, re, re) + 1024);
   } else {
@@ -506,12 +524,17 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     }
   }
   for (int attempt = 0; attempt < 4; ++attempt) {
-    a.out.ranks = out.ranks.p;
-    a.out.off = out.off.p;
+    a.out.ranks = out.ranks.p + (append ? 2 * obase : 0);
+    a.out.off = out.off.p + (append ? obase : 0);
     a.out.base = out.arena.p;
     a.out.used = reinterpret_cast<unsigned long long*>(c->d_status.p + kStWords);
     a.out.capacity = (long long)out.arena.n;
     CK(cudaMemsetAsync(c->d_status.p, 0, (kStWords + 4) * sizeof(int), c->st));
+    if (append) {  // the bump counter starts after the entries already placed
+      c->h_base_used = (unsigned long long)base_used;
+      CK(cudaMemcpyAsync(a.out.used, &c->h_base_used, sizeof(unsigned long long),
+                         cudaMemcpyHostToDevice, c->st));
+    }
     CK(cudaMemsetAsync(c->d_acc.p, 0, 2 * kAccSlots * sizeof(double), c->st));
     if (use_tsqr) {
       a.RM1 = RM1;
@@ -565,13 +588,19 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
         *reinterpret_cast<unsigned long long*>(c->h_status + kStWords);
     if (c->h_status[kStOverflow]) {
       const size_t want = std::max<size_t>(out.arena.n + 1024, (size_t)(used * 1.5) + 1024);
-      out.arena.free();
-      out.arena.alloc(want);
+      if (append) {
+        grow_preserve(c, out, base_used, (long long)want);
+      } else {
+        out.arena.free();
+        out.arena.alloc(want);
+      }
       continue;
     }
     out.used = (long long)used;
-    out.maxr1 = c->h_status[kStMaxR1] > 0 ? c->h_status[kStMaxR1] : 1;
-    out.maxr2 = c->h_status[kStMaxR2] > 0 ? c->h_status[kStMaxR2] : 1;
+    const int m1 = c->h_status[kStMaxR1] > 0 ? c->h_status[kStMaxR1] : 1;
+    const int m2 = c->h_status[kStMaxR2] > 0 ? c->h_status[kStMaxR2] : 1;
+    out.maxr1 = append ? std::max(out.maxr1, m1) : m1;
+    out.maxr2 = append ? std::max(out.maxr2, m2) : m2;
     if (c->h_status[kStError])
       throw Fail{TTDVM_EDOMAIN, "rounding: non-finite input in output " +
                                     std::to_string(c->h_status[kStErrIdx])};
@@ -1071,6 +1100,7 @@ void build_step_terms(ttdvm_ctx* c) {
   }
   ul.upload();
   c->terms_dirty = false;
+  c->built_blocks = 0;  // per-block lists follow the global ones
 }
 
 // Grow an arena to hold `need` doubles, preserving its first `keep` doubles.
@@ -1116,6 +1146,116 @@ void append_tensors(ttdvm_ctx* c, const TSet& src, const int* src_ids_dev, int c
   dst.maxr2 = m2;
 }
 
+// Per-block summand lists of the blocked step, derived from the global
+// ones (same summands, same order, so every output is the same sum): block b
+// owns cells [blk_c0[b], blk_c0[b+1]); its flux list holds the faces those
+// cells touch (cut faces are rounded in both adjacent blocks), its residual
+// list points into that local flux set, its update list into the local
+// residual set.
+void build_block_terms(ttdvm_ctx* c) {
+  const int nb = c->nblocks;
+  if (c->built_blocks == nb) return;
+  const int nown = c->nowned < 0 ? c->ncell : c->nowned;
+  for (auto* v : {&c->bt_flux, &c->bt_res, &c->bt_upd})
+    for (TermList& t : *v) t.free();
+  c->bt_flux.assign(nb, TermList());
+  c->bt_res.assign(nb, TermList());
+  c->bt_upd.assign(nb, TermList());
+  c->blk_c0.assign(nb + 1, 0);
+  for (int b = 0; b <= nb; ++b) c->blk_c0[b] = (int)((long long)nown * b / nb);
+  std::vector<int> pos(c->nface, -1);
+  for (int b = 0; b < nb; ++b) {
+    const int c0 = c->blk_c0[b], c1 = c->blk_c0[b + 1];
+    TermList& fl = c->bt_flux[b];
+    TermList& rl = c->bt_res[b];
+    TermList& ul = c->bt_upd[b];
+    fl.off.assign(1, 0);
+    rl.off.assign(1, 0);
+    ul.off.assign(1, 0);
+    std::vector<int> faces;
+    for (int i = c0; i < c1; ++i)
+      for (long long e = c->cfo[i]; e < c->cfo[i + 1]; ++e) {
+        const int fid = c->cfid[e];
+        if (pos[fid] >= 0) continue;
+        pos[fid] = (int)faces.size();
+        faces.push_back(fid);
+        for (long long k = c->t_flux.off[fid]; k < c->t_flux.off[fid + 1]; ++k)
+          fl.terms.push_back(c->t_flux.terms[k]);
+        fl.off.push_back((long long)fl.terms.size());
+      }
+    for (int i = c0; i < c1; ++i) {
+      for (long long k = c->t_res.off[i]; k < c->t_res.off[i + 1]; ++k) {
+        Term t = c->t_res.terms[k];
+        if (t.set == S_PHI) t.idx = pos[t.idx];
+        rl.terms.push_back(t);
+      }
+      rl.off.push_back((long long)rl.terms.size());
+      for (long long k = c->t_upd.off[i]; k < c->t_upd.off[i + 1]; ++k) {
+        Term t = c->t_upd.terms[k];
+        if (t.set == S_RES) t.idx -= c0;
+        ul.terms.push_back(t);
+      }
+      ul.off.push_back((long long)ul.terms.size());
+    }
+    for (int fid : faces) pos[fid] = -1;
+    fl.upload();
+    rl.upload();
+    ul.upload();
+  }
+  c->built_blocks = nb;
+}
+
+// Pieces (1), (2) and the time update of one step, blocked when nblocks > 1.
+void step_fluxes_updates(ttdvm_ctx* c, TensorSet& s, TensorSet& nxt, double dt, double eps,
+                         int cap) {
+  TensorSet* sets[kMaxSets] = {&s,         &c->fsraw,      &c->fs, &c->jr,  &c->phi,
+                                &c->res,    &c->freestream, &c->in, &c->xin, &c->eabs};
+  {
+    Timer t(c, 4);
+    run_walls(c, s, 0);
+  }
+  if (c->nblocks <= 1) {
+    {
+      Timer t(c, 4);
+      run_round(c, c->t_flux, sets, c->phi, eps, cap, nullptr);
+    }
+    c->res.uscale = 1.0;
+    {
+      Timer t(c, 5);
+      run_round(c, c->t_res, sets, c->res, eps, cap, nullptr);
+    }
+    c->res.uscale = dt;
+    nxt.resize(c->ncell);
+    {
+      Timer t(c, 6);
+      run_round(c, c->t_upd, sets, nxt, eps, cap, nullptr);
+    }
+    c->res.uscale = 1.0;
+    return;
+  }
+  build_block_terms(c);
+  nxt.resize(c->ncell);
+  nxt.used = 0;
+  nxt.maxr1 = nxt.maxr2 = 1;
+  for (int b = 0; b < c->nblocks; ++b) {
+    {
+      Timer t(c, 4);
+      run_round(c, c->bt_flux[b], sets, c->phi, eps, cap, nullptr);
+    }
+    c->res.uscale = 1.0;
+    {
+      Timer t(c, 5);
+      run_round(c, c->bt_res[b], sets, c->res, eps, cap, nullptr);
+    }
+    c->res.uscale = dt;
+    {
+      Timer t(c, 6);
+      run_round(c, c->bt_upd[b], sets, nxt, eps, cap, nullptr, c->blk_c0[b]);
+    }
+    c->res.uscale = 1.0;
+  }
+}
+
 void step_once(ttdvm_ctx* c, double dt, double eps, int cap) {
   TensorSet& s = c->state[c->cur];
   TensorSet& nxt = c->state[1 - c->cur];
@@ -1125,23 +1265,22 @@ void step_once(ttdvm_ctx* c, double dt, double eps, int cap) {
   // rounding, physics.cpp:118)
   run_collision(c, s, eps, nown);
   c->jr.tscale = c->d_nu.p;
-  TensorSet* sets[kMaxSets] = {&s,         &c->fsraw,      &c->fs, &c->jr,  &c->phi,
-                                &c->res,    &c->freestream, &c->in, &c->xin, &c->eabs};
-  {
-    Timer t(c, 4);
-    run_walls(c, s, 0);
-    run_round(c, c->t_flux, sets, c->phi, eps, cap, nullptr);
-  }
-  c->res.uscale = 1.0;
-  {
-    Timer t(c, 5);
-    run_round(c, c->t_res, sets, c->res, eps, cap, nullptr);
-  }
-  c->res.uscale = dt;
-  nxt.resize(c->ncell);
-  {
-    Timer t(c, 6);
-    run_round(c, c->t_upd, sets, nxt, eps, cap, nullptr);
+  for (;;) {
+    try {
+      step_fluxes_updates(c, s, nxt, dt, eps, cap);
+      break;
+    } catch (const Fail& e) {
+      // out of device memory: release the flux / residual / next-state
+      // arenas and redo pieces (1), (2) and the update in 4x more cell
+      // blocks (the state and J_r are untouched, so the step is unchanged)
+      if (e.code != TTDVM_ENOMEM || !c->auto_blocks || c->nblocks >= 256 || nown < 8 * c->nblocks)
+        throw;
+      c->phi.free();
+      c->res.free();
+      nxt.arena.free();
+      nxt.used = 0;
+      c->nblocks *= 4;
+    }
   }
   c->res.uscale = 1.0;
   nxt.count = c->ncell;
@@ -1557,18 +1696,27 @@ int ttdvm_cuda_wall_densities(ttdvm_ctx* c, double* out) {
   });
 }
 
-int ttdvm_cuda_setup_info(ttdvm_ctx* c, int64_t* info4) {
+int ttdvm_cuda_setup_info(ttdvm_ctx* c, int64_t* info5) {
   return guard(c, [&] {
-    info4[0] = c->n_oblique;
-    info4[1] = c->noise_floor;
-    info4[2] = c->nwall;
-    info4[3] = (int64_t)(c->ff_ms * 1000.0);
+    info5[0] = c->n_oblique;
+    info5[1] = c->noise_floor;
+    info5[2] = c->nwall;
+    info5[3] = (int64_t)(c->ff_ms * 1000.0);
+    info5[4] = c->nblocks;
   });
 }
 
 int ttdvm_cuda_phase_times(ttdvm_ctx* c, double* ms8) {
   return guard(c, [&] {
     for (int i = 0; i < 8; ++i) ms8[i] = c->phase_ms[i];
+  });
+}
+
+int ttdvm_cuda_set_blocks(ttdvm_ctx* c, int32_t nblocks) {
+  return guard(c, [&] {
+    require(nblocks >= 0, "set_blocks: nblocks must be >= 0");
+    c->auto_blocks = nblocks == 0;
+    c->nblocks = std::max(1, (int)nblocks);
   });
 }
 

@@ -33,7 +33,7 @@ EXPORTS = (
     "ttdvm_cuda_macro_batch", "ttdvm_cuda_collision_batch", "ttdvm_cuda_phase_times",
     "ttdvm_cuda_launch_count", "ttdvm_cuda_set_profiling", "ttdvm_cuda_phase_work",
     "ttdvm_cuda_timed_step", "ttdvm_cuda_fp64_peak", "ttdvm_cuda_round_profile",
-    "ttdvm_cuda_set_owned", "ttdvm_cuda_halo_pack", "ttdvm_cuda_halo_unpack",
+    "ttdvm_cuda_set_owned", "ttdvm_cuda_set_blocks", "ttdvm_cuda_halo_pack", "ttdvm_cuda_halo_unpack",
     "ttdvm_cuda_face_factors", "ttdvm_cuda_wall_densities", "ttdvm_cuda_setup_info",
     "ttdvm_cuda_round_resident",
 )
@@ -94,6 +94,7 @@ def load_library(path: str = LIB_PATH):
         "ttdvm_cuda_fp64_peak": (C.c_int, [vp, vp]),
         "ttdvm_cuda_round_profile": (C.c_int, [vp, C.c_int, vp]),
         "ttdvm_cuda_set_owned": (C.c_int, [vp, i32]),
+        "ttdvm_cuda_set_blocks": (C.c_int, [vp, i32]),
         "ttdvm_cuda_halo_pack": (C.c_int, [vp, i32, vp, vp, vp, vp, i64]),
         "ttdvm_cuda_halo_unpack": (C.c_int, [vp, i32, vp, vp, vp, vp]),
         "ttdvm_cuda_face_factors": (C.c_int, [vp, i32, vp, i32, i32, vp]),
@@ -229,6 +230,10 @@ class Context:
         """explicit_step, nsteps times, state resident."""
         self._check(self.lib.ttdvm_cuda_step(self.h, float(dt), float(eps), int(cap), int(nsteps)))
 
+    def set_blocks(self, nblocks: int):
+        """Cell blocks of the bounded-memory step (0 = automatic)."""
+        self._check(self.lib.ttdvm_cuda_set_blocks(self.h, int(nblocks)))
+
     def set_owned(self, nowned: int):
         """Cells [0, nowned) are stepped; the rest are halo ghosts."""
         self._check(self.lib.ttdvm_cuda_set_owned(self.h, int(nowned)))
@@ -333,10 +338,11 @@ class Context:
         return out
 
     def setup_info(self) -> dict:
-        info = np.zeros(4, dtype=np.int64)
+        info = np.zeros(5, dtype=np.int64)
         self._check(self.lib.ttdvm_cuda_setup_info(self.h, _ptr(info)))
         return dict(oblique_normals=int(info[0]), noise_floor_normals=int(info[1]),
-                    wall_faces=int(info[2]), face_factor_ms=float(info[3]) / 1000.0)
+                    wall_faces=int(info[2]), face_factor_ms=float(info[3]) / 1000.0,
+                    cell_blocks=int(info[4]))
 
     def wall_densities(self) -> np.ndarray:
         """n_w of the last step per wall face, in face order."""

@@ -424,3 +424,23 @@ def test_round_batch_edge_inputs(ctx):
     assert rel_err(got.full(0), ts[0].to_full()) < 1e-11
     with pytest.raises(ValueError):
         ctx.rounded(TtBatch.from_list(ts[:2]), 1e-8, group_off=[0, 0, 2])  # an empty sum
+
+
+@pytest.mark.parametrize("cfg,scale,blocks", [(2, 4 / 32, 3), (4, 0.1, 5)])
+def test_blocked_step_matches_one_block(ctx, cfg, scale, blocks):
+    """ttdvm_cuda_set_blocks: the bounded-memory step (fluxes, residuals and
+    updates of contiguous cell blocks) forms the same sums as the one-block
+    step, so states agree to roundoff with identical ranks."""
+    p = config(cfg, scale)
+    res = []
+    for nb in (1, blocks):
+        ctx.setup(p)
+        ctx.set_blocks(nb)
+        ctx.step(p.dt, p.eps, p.cap, 2)
+        res.append((ctx.download_state(), ctx.macros()))
+    ctx.set_blocks(0)
+    (a, ma), (b, mb) = res
+    np.testing.assert_array_equal(a.ranks, b.ranks)
+    for i in range(p.mesh.ncell):
+        assert rel_err(b.full(i), a.full(i)) <= 1e-12, i
+    np.testing.assert_allclose(mb, ma, rtol=1e-12, atol=1e-14)
