@@ -6,23 +6,6 @@
 
 namespace ttdvm {
 
-namespace {
-constexpr int MT = 128;  // threads per cell
-
-__device__ double msum(double v, double* red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  double s = 0.0;
-#pragma unroll
-  for (int w = 0; w < MT / 32; ++w) s += red[w];
-  return s;
-}
-}  // namespace
-
 struct MacroArgs {
   TSet set;
   int count, n;
@@ -36,14 +19,43 @@ struct MacroArgs {
 
 // compute_macro (proj/src/physics.cpp:17-67).  Each of the reference's 16
 // convolutions (tt_tensor.cpp:195-204) is u^T first * (sum_j v_j M_j) *
-// last w; the three per-axis weight families are contracted with the cores
-// once per pass.  Pass 1 uses {w, xi w, xi^2 w} (n, n u, e2); pass 2 the
+// last w; the per-axis weight families are contracted with the cores once
+// per pass.  Pass 1 uses {w, xi w, xi^2 w} (n, n u, e2); pass 2 the
 // c-shifted {w, c w, c^2 w, c^3 w} of each axis (S), exactly the weights the
-// reference builds (physics.cpp:44-61).  One CTA per tensor; the middle core
-// is streamed with coalesced loads (HBM-bound).
-__global__ void __launch_bounds__(MT) macro_kernel(MacroArgs p) {
-  const int c = blockIdx.x;
-  if (c >= p.count) return;
+// reference builds (physics.cpp:44-61).
+//
+// One warp per tensor, MW tensors per CTA, no block barriers: the first- and
+// last-core contractions a1[q][a] = sum_i W_q(x_i) F(i,a) and
+// a3[q][b] = sum_k L(b,k) W_q(x_k) run with lanes over the nodes (warp
+// reductions); the middle-core contraction and the bilinear forms
+// sum_{a,b} a1[p][a] (sum_j W_q(x_j) M_j(a,b)) a3[r][b] run with lanes over
+// (entry, slice) pairs -- all 32 lanes busy even for rank-1 tensors -- and the
+// middle contraction is never stored (the forms are linear in it).  HBM-bound:
+// every core is read once per pass with coalesced loads.
+constexpr int MW = 4;  // tensors (warps) per CTA
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// weight q of an axis at node x: pass 0: {1, x, x^2} w; pass 1: c^q w with
+// c = (x - u) / s
+__device__ __forceinline__ void weights4(int pass, double x, double w, double u, double inv_s,
+                                         double (&W)[4]) {
+  const double c = pass == 0 ? x : (x - u) * inv_s;
+  W[0] = w;
+  W[1] = c * w;
+  W[2] = c * W[1];
+  W[3] = pass == 0 ? 0.0 : c * W[2];
+}
+
+__global__ void __launch_bounds__(32 * MW) macro_kernel(MacroArgs p) {
+  __shared__ double s_a[MW][8 * 64];  // per warp: a1 [4][r1], a3 [4][r2] (r <= 64)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c = blockIdx.x * MW + wid;
+  if (c >= p.count) return;  // warp-uniform
   const int n = p.n;
   const int r1 = p.set.ranks[2 * c], r2 = p.set.ranks[2 * c + 1];
   const double* F = p.set.base + p.set.off[c];
@@ -51,154 +63,130 @@ __global__ void __launch_bounds__(MT) macro_kernel(MacroArgs p) {
   const double* L = M + (long long)n * r1 * r2;
   double sc = p.set.uscale;
   if (p.set.tscale) sc *= p.set.tscale[c];
-
-  extern __shared__ double sm[];
-  // weights wa[axis][4][n]
-  double* wa = sm;                 // 3*4*n
-  double* a1 = wa + 12 * n;        // 4 x r1
-  double* a3 = a1 + 4 * r1;        // 4 x r2
-  double* bm = a3 + 4 * r2;        // 4 x r1 x r2
-  __shared__ double red[MT / 32];
-  __shared__ double mac[16];
-
+  double* a1 = s_a[wid];
+  double* a3 = a1 + 4 * r1;
   const double R = p.gas[1];
+  const int P0[7][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {2, 0, 0}, {0, 2, 0}, {0, 0, 2}};
+  const int P1[9][3] = {{3, 0, 0}, {1, 2, 0}, {1, 0, 2}, {2, 1, 0}, {0, 3, 0},
+                        {0, 1, 2}, {2, 0, 1}, {0, 2, 1}, {0, 0, 3}};
+  double nd = 0.0, u[3] = {0.0, 0.0, 0.0}, T = 0.0, inv_s = 0.0, S[3];
+  const int rr = r1 * r2;
+  // lanes per (entry, slice) group of the middle contraction
+  const int lpe = rr >= 32 ? 1 : 32 / rr;
+  const int eg = lane / lpe, js = lane - eg * lpe;
+  const int estep = 32 / lpe;
   for (int pass = 0; pass < 2; ++pass) {
-    // ---- weights ----
-    for (int i = threadIdx.x; i < n; i += MT) {
-      const double w = p.weights[i], x = p.nodes[i];
-      for (int ax = 0; ax < 3; ++ax) {
-        double* W = wa + ax * 4 * n;
-        if (pass == 0) {
-          const double xw = x * w;
-          W[i] = w;
-          W[n + i] = xw;
-          W[2 * n + i] = x * xw;
-          W[3 * n + i] = 0.0;
-        } else {
-          const double cc = (x - mac[1 + ax]) / mac[8];
-          const double cw = cc * w, c2w = cc * cw;
-          W[i] = w;
-          W[n + i] = cw;
-          W[2 * n + i] = c2w;
-          W[3 * n + i] = cc * c2w;
-        }
-      }
-    }
-    __syncthreads();
     const int nw = pass == 0 ? 3 : 4;
-    // a1[p][a] = sum_i W0[p][i] F(i,a) (scale folded here, as scaled() does)
-    for (int e = threadIdx.x; e < nw * r1; e += MT) {
-      const int q = e / r1, a = e % r1;
-      const double* W = wa + q * n;
-      double s = 0.0;
-      for (int i = 0; i < n; ++i) s += W[i] * (sc * F[i + n * a]);
-      a1[q * r1 + a] = s;
-    }
-    for (int e = threadIdx.x; e < nw * r2; e += MT) {
-      const int q = e / r2, b = e % r2;
-      const double* W = wa + 2 * 4 * n + q * n;
-      double s = 0.0;
-      for (int k = 0; k < n; ++k) s += L[b + r2 * k] * W[k];
-      a3[q * r2 + b] = s;
-    }
-    for (int e = threadIdx.x; e < r1 * r2; e += MT) {
-      const double* W = wa + 4 * n;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      for (int j = 0; j < n; ++j) {
-        const double m = M[(long long)j * r1 * r2 + e];
-        s0 += W[j] * m;
-        s1 += W[n + j] * m;
-        s2 += W[2 * n + j] * m;
-        s3 += W[3 * n + j] * m;
+    // a1[q][a] = sum_i W_q(x_i) sc F(i, a); a3[q][b] = sum_k L(b, k) W_q(x_k)
+    for (int a = 0; a < r1; ++a) {
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int i = lane; i < n; i += 32) {
+        double W[4];
+        weights4(pass, p.nodes[i], p.weights[i], u[0], inv_s, W);
+        const double v = sc * F[i + n * a];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s4[q] += W[q] * v;
       }
-      bm[e] = s0;
-      bm[r1 * r2 + e] = s1;
-      bm[2 * r1 * r2 + e] = s2;
-      bm[3 * r1 * r2 + e] = s3;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < nw) {
+          const double t = wsum(s4[q]);
+          if (lane == 0) a1[q * r1 + a] = t;
+        }
     }
-    __syncthreads();
-    // bilinear forms conv(p,q,r) = a1[p] . bm[q] . a3[r]
+    for (int b = 0; b < r2; ++b) {
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = lane; k < n; k += 32) {
+        double W[4];
+        weights4(pass, p.nodes[k], p.weights[k], u[2], inv_s, W);
+        const double v = L[b + r2 * k];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s4[q] += v * W[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < nw) {
+          const double t = wsum(s4[q]);
+          if (lane == 0) a3[q * r2 + b] = t;
+        }
+    }
+    __syncwarp();
+    // bilinear forms conv(p,q,r) = a1[p] . (sum_j W_q(x_j) M_j) . a3[r]
     // pass 0: (000) (100) (010) (001) (200) (020) (002)
     // pass 1: S0: (300) (120) (102); S1: (210) (030) (012); S2: (201) (021) (003)
     const int nf = pass == 0 ? 7 : 9;
-    const int P0[7][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {2, 0, 0}, {0, 2, 0}, {0, 0, 2}};
-    const int P1[9][3] = {{3, 0, 0}, {1, 2, 0}, {1, 0, 2}, {2, 1, 0}, {0, 3, 0},
-                          {0, 1, 2}, {2, 0, 1}, {0, 2, 1}, {0, 0, 3}};
     double part[9];
 #pragma unroll
     for (int f = 0; f < 9; ++f) part[f] = 0.0;
-    for (int e = threadIdx.x; e < r1 * r2; e += MT) {
-      const int a = e % r1, b = e / r1;
+    if (eg < estep) {
+      for (int e = eg; e < rr; e += estep) {
+        double bm[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int j = js; j < n; j += lpe) {
+          double W[4];
+          weights4(pass, p.nodes[j], p.weights[j], u[1], inv_s, W);
+          const double m = M[(long long)j * rr + e];
 #pragma unroll
-      for (int f = 0; f < 9; ++f) {
-        if (f < nf) {
-          const int* q = pass == 0 ? P0[f] : P1[f];
-          part[f] += a1[q[0] * r1 + a] * bm[q[1] * r1 * r2 + e] * a3[q[2] * r2 + b];
+          for (int q = 0; q < 4; ++q) bm[q] += W[q] * m;
         }
+        const int a = e % r1, b = e / r1;
+#pragma unroll
+        for (int f = 0; f < 9; ++f)
+          if (f < nf) {
+            const int* q = pass == 0 ? P0[f] : P1[f];
+            part[f] += a1[q[0] * r1 + a] * bm[q[1]] * a3[q[2] * r2 + b];
+          }
       }
     }
     double tot[9];
 #pragma unroll
-    for (int f = 0; f < 9; ++f) tot[f] = f < nf ? msum(part[f], red) : 0.0;
-    if (threadIdx.x == 0) {
-      if (pass == 0) {
-        const double nd = tot[0];
-        mac[0] = nd;
-        int err = 0;
-        if (!(nd > 0.0)) err = kErrDensity;
-        const double u0 = tot[1] / nd, u1 = tot[2] / nd, u2 = tot[3] / nd;
-        const double e2 = tot[4] + tot[5] + tot[6];
-        const double T = (e2 - nd * (u0 * u0 + u1 * u1 + u2 * u2)) / (3.0 * nd * R);
-        if (!err && !(T > 0.0)) err = kErrTemperature;
-        mac[1] = u0;
-        mac[2] = u1;
-        mac[3] = u2;
-        mac[4] = T;
-        mac[8] = err ? 1.0 : sqrt(2.0 * R * T);
-        mac[9] = err;
-        if (err && atomicCAS(&p.status[kStError], 0, err) == 0) p.status[kStErrIdx] = c;
-      } else {
-        const double nd = mac[0];
-        mac[5] = (tot[0] + tot[1] + tot[2]) / nd;
-        mac[6] = (tot[3] + tot[4] + tot[5]) / nd;
-        mac[7] = (tot[6] + tot[7] + tot[8]) / nd;
+    for (int f = 0; f < 9; ++f) tot[f] = f < nf ? wsum(part[f]) : 0.0;
+    __syncwarp();  // a1 / a3 are rewritten by the next pass
+    if (pass == 0) {
+      nd = tot[0];
+      int err = 0;
+      if (!(nd > 0.0)) err = kErrDensity;
+      u[0] = tot[1] / nd;
+      u[1] = tot[2] / nd;
+      u[2] = tot[3] / nd;
+      const double e2 = tot[4] + tot[5] + tot[6];
+      T = (e2 - nd * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2])) / (3.0 * nd * R);
+      if (!err && !(T > 0.0)) err = kErrTemperature;
+      if (err) {  // blow-up reported; no S for this tensor
+        if (lane == 0 && atomicCAS(&p.status[kStError], 0, err) == 0) p.status[kStErrIdx] = c;
+        return;
       }
+      inv_s = 1.0 / sqrt(2.0 * R * T);
+    } else {
+      S[0] = (tot[0] + tot[1] + tot[2]) / nd;
+      S[1] = (tot[3] + tot[4] + tot[5]) / nd;
+      S[2] = (tot[6] + tot[7] + tot[8]) / nd;
     }
-    __syncthreads();
-    if (mac[9] != 0.0) return;  // blow-up reported; no S for this cell
   }
-  if (threadIdx.x == 0) {
-    const double m = p.gas[0], T = mac[4];
-    const double rho = m * mac[0];
+  if (lane == 0) {
+    const double m = p.gas[0];
+    const double rho = m * nd;
     const double pr = rho * R * T;
     const double mu = p.gas[3] * pow(T / p.gas[4], p.gas[5]);
     double* out = p.macro + 11LL * c;
-    out[0] = mac[0];
-    out[1] = mac[1];
-    out[2] = mac[2];
-    out[3] = mac[3];
+    out[0] = nd;
+    out[1] = u[0];
+    out[2] = u[1];
+    out[3] = u[2];
     out[4] = T;
     out[5] = rho;
     out[6] = pr;
-    out[7] = mac[5];
-    out[8] = mac[6];
-    out[9] = mac[7];
+    out[7] = S[0];
+    out[8] = S[1];
+    out[9] = S[2];
     out[10] = pr / mu;
     if (p.nu) p.nu[c] = pr / mu;
   }
 }
 
-size_t macro_smem_bytes(int n, int rmax) {
-  return 8 * (size_t)(12 * n + 4 * rmax + 4 * rmax + 4 * rmax * rmax);
-}
-
 cudaError_t launch_macro(const MacroArgs& a, int rmax, cudaStream_t st) {
   if (a.count == 0) return cudaSuccess;
-  const size_t smem = macro_smem_bytes(a.n, rmax);
-  cudaError_t e =
-      cudaFuncSetAttribute(macro_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  macro_kernel<<<a.count, MT, smem, st>>>(a);
+  if (rmax > 64) return cudaErrorInvalidValue;  // ranks are <= n <= 64
+  macro_kernel<<<(a.count + MW - 1) / MW, 32 * MW, 0, st>>>(a);
   return cudaGetLastError();
 }
 
