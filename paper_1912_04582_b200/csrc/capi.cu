@@ -43,6 +43,9 @@ TTDVM_GRAM_API
 namespace g256 {
 TTDVM_GRAM_API
 }
+namespace g32 {
+TTDVM_GRAM_API
+}
 #undef TTDVM_GRAM_API
 using g128::round_gram_smem_bytes;  // the plan does not depend on the CTA width
 using g128::round_gram_spill_doubles;
@@ -444,7 +447,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   constexpr size_t kSmemMax = 227 * 1024;
   struct Launch {
     int bin, count, rm1, rm2, ms, jb;
-    bool spill, wide;
+    bool spill, wide, narrow;
   };
   // 256-thread CTAs from Gram dimension TTDVM_WIDE_D (default 16) up: the
   // measured crossover between the short-phase small tiles (128 threads, four
@@ -453,12 +456,22 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     const char* e = getenv("TTDVM_WIDE_D");
     return e ? atoi(e) : 16;
   }();
+  // one-warp CTAs (round32.cu) up to Gram dimension TTDVM_NARROW_D (default
+  // 4).  Measured on config 4 (same box, half scale): the rank-<=4 bins --
+  // all f_S roundings, most collision and update sums -- run 30-45 % faster
+  // than on 128-thread CTAs; the (4, 8] bins lose a little on the updates,
+  // and (8, 12] (the face fluxes) run 2.4x slower.
+  static const int narrow_d = [] {
+    const char* e = getenv("TTDVM_NARROW_D");
+    return e ? atoi(e) : 4;
+  }();
   auto gram_d = [&](int rm1, int rm2) { return std::max(std::min(n, rm1), std::min(n, rm2)); };
   // CTAs per SM the kernel variant is built for (its launch bounds)
   auto blocks_per_sm = [&](int rm1, int rm2) {
     const int d = gram_d(rm1, rm2);
     const int ne = d * (d + 1) / 2;
     if (d >= wide_d) return ne <= 3 * 256 ? 2 : 1;
+    if (d <= narrow_d) return 12;  // one-warp CTAs: many outputs per SM
     if (d <= g128::round_gram_tiny_d()) return g128::round_gram_tiny_minb();  // its launch bounds
     return ne <= 3 * 128 ? 4 : (ne <= 10 * 128 ? 3 : 1);
   };
@@ -478,13 +491,15 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     if (!bcount[b]) continue;
     const int* bm = bmax + kBinWords * b;
     Launch l{b, bcount[b], std::max(1, bm[0]), std::max(1, bm[1]), std::max(1, bm[2]), 1, false,
-             false};
+             false, false};
     l.wide = gram_d(l.rm1, l.rm2) >= wide_d;
+    l.narrow = !l.wide && gram_d(l.rm1, l.rm2) <= narrow_d;
     // working sets above the shared-memory budget (n = 64, summed ranks of
     // ~100 and more) take the spill plan: F, last^T, XP and the Gram region
     // in a per-CTA global scratch slice, persistent CTAs
     l.spill = !use_tsqr &&
               round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false) > kSmemMax;
+    if (l.spill) l.narrow = false;
     if (!use_tsqr && !l.spill) l.jb = pick_jb(l);
     static const int force_jb = [] {  // diagnostics: TTDVM_JB=k forces k slices per phase
       const char* e = getenv("TTDVM_JB");
@@ -564,8 +579,9 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
           c->d_gscratch.alloc((size_t)grid * (size_t)a.gstride);
           a.gscratch = c->d_gscratch.p;
         }
-        CK(l.wide ? g256::launch_round_gram(a, grid, c->st)
-                  : g128::launch_round_gram(a, grid, c->st));
+        CK(l.wide     ? g256::launch_round_gram(a, grid, c->st)
+           : l.narrow ? g32::launch_round_gram(a, grid, c->st)
+                      : g128::launch_round_gram(a, grid, c->st));
         c->launches += 1;
       }
     }

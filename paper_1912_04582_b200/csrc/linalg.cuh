@@ -16,7 +16,8 @@ namespace {
 #ifndef TTDVM_ROUND_NT
 #define TTDVM_ROUND_NT 128
 #endif
-static_assert(TTDVM_ROUND_NT == kRoundThreads || TTDVM_ROUND_NT == 256, "CTA width");
+static_assert(TTDVM_ROUND_NT == kRoundThreads || TTDVM_ROUND_NT == 256 || TTDVM_ROUND_NT == 32,
+              "CTA width");
 constexpr int NT = TTDVM_ROUND_NT;
 constexpr int NW = NT / 32;
 

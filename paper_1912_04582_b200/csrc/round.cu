@@ -1064,6 +1064,8 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
 // n = 64) on 256 (more threads per dense slice product).
 #if TTDVM_ROUND_NT == 256
 #define RG_NS g256
+#elif TTDVM_ROUND_NT == 32
+#define RG_NS g32
 #else
 #define RG_NS g128
 #endif
