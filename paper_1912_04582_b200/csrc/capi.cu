@@ -530,12 +530,12 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   } else {
     // headroom: ranks drift upward from step to step; an arena that held
     // this set's previous result with less than 25 % to spare is regrown
-    // (its content is dead) to 60 % above it, so neither the overflow-and-
-    // repeat path below nor the regrowth itself (a multi-GB cudaFree +
-    // cudaMalloc, hundreds of ms) recurs every step as the ranks creep up
+    // (its content is dead) to twice it, so neither the overflow-and-repeat
+    // path below nor the regrowth itself (a multi-GB cudaFree + cudaMalloc,
+    // up to hundreds of ms) recurs step after step as the ranks creep up
     if ((double)out.arena.n < (double)out.used * 1.25 + 1024) {
       out.arena.free();
-      out.arena.alloc((size_t)((double)out.used * 1.6) + 1024);
+      out.arena.alloc((size_t)((double)out.used * 2.0) + 1024);
     }
   }
   for (int attempt = 0; attempt < 4; ++attempt) {

@@ -428,7 +428,10 @@ __device__ __noinline__ int svd_from_r(const double* R, int ldr, int k, int m, c
 // the call (other CTAs keep the SM busy).  Same arithmetic as the block
 // versions, same results.
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kWarpMaxD = 16;  // measured: the block versions win from ~24 up
+#ifndef TTDVM_WARP_MAX_D
+#define TTDVM_WARP_MAX_D 16
+#endif
+constexpr int kWarpMaxD = TTDVM_WARP_MAX_D;  // measured: the block versions win from ~24 up
 
 // chol_piv_dd on warp 0 (d <= 32): lane v holds virtual column v's pivot;
 // row k of R is formed by lane v (> k) and broadcast by shuffles for the
