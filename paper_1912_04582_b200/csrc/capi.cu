@@ -477,11 +477,15 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   };
   // slices per barrier phase: about a quarter of the slices (measured best
   // on config 4: fewer phases pay for a lower CTA count), shrunk while the
-  // plan would leave fewer CTAs per SM than the variant's launch bounds
+  // plan would leave fewer CTAs per SM than the variant's launch bounds --
+  // or than the JB = 1 plan itself fits (then the spare shared memory goes
+  // to larger slice batches: config 3, +6 %)
   auto pick_jb = [&](const Launch& l) {
     const size_t base = round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false);
+    const int fit1 = std::max(1, (int)(228 * 1024 / (base + 1024)));
+    const int k = std::min(blocks_per_sm(l.rm1, l.rm2), fit1);
     const size_t budget =
-        std::max(base, (size_t)(228 * 1024 / blocks_per_sm(l.rm1, l.rm2)) - 2048);
+        std::max(base, std::min(kSmemMax, (size_t)(228 * 1024 / k) - 2048));
     int jb = (n + 3) / 4;
     while (jb > 1 && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, jb, false) > budget) --jb;
     return jb;
