@@ -16,6 +16,9 @@
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
+#include <chrono>
+#include <mutex>
+#include <vector>
 #include <string>
 #include <array>
 #include <unordered_map>
@@ -125,27 +128,80 @@ struct Fail {
       throw Fail{TTDVM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};      \
   } while (0)
 
+// Deferred device frees.  cudaFree synchronises the device and, measured on
+// the box with ~10-50 GB allocated, costs 0.2-0.5 s whatever the block size;
+// arenas regrown inside a step therefore park their old block here
+// (DevBuf::retire) instead of freeing it.  Parked blocks are freed when an
+// allocation fails (then retried once) and when a context is destroyed.  The
+// parked total stays below the live arenas' own size (each regrowth at least
+// doubles).  TTDVM_DEFER_FREE=0 restores immediate frees (A/B).
+std::mutex g_park_mu;
+std::vector<void*> g_parked;
+bool defer_free_on() {
+  static const bool on = [] {
+    const char* e = getenv("TTDVM_DEFER_FREE");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+bool flush_parked() {
+  std::vector<void*> v;
+  {
+    std::lock_guard<std::mutex> lk(g_park_mu);
+    v.swap(g_parked);
+  }
+  if (v.empty()) return false;
+  cudaDeviceSynchronize();
+  for (void* q : v) cudaFree(q);
+  return true;
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  // A regrowth (a block already held) parks the old block and takes 1.5x
+  // headroom, so buffers that creep up step by step (spill scratch, bin
+  // lists) neither cudaFree inside a step nor regrow every step.
   void alloc(size_t count) {
     if (count <= n && p) return;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
+    const bool regrow = p != nullptr;
+    retire();
     if (count == 0) return;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    const size_t want = regrow ? count + count / 2 : count;
+    cudaError_t e = cudaMalloc(&p, want * sizeof(T));
     if (e != cudaSuccess) {
       cudaGetLastError();
+      flush_parked();
+      e = cudaMalloc(&p, count * sizeof(T));
+      if (e == cudaSuccess) n = count;
+    } else {
+      n = want;
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      n = 0;
       throw Fail{TTDVM_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes"};
     }
-    n = count;
   }
   void free() {
     if (p) cudaFree(p);
     p = nullptr;
     n = 0;
+  }
+  // free without a device synchronisation inside a step (see g_parked); the
+  // caller guarantees no pending work still reads the block's content
+  // beyond the stream order (parked blocks are only freed after a device sync)
+  void retire() {
+    if (p && defer_free_on()) {
+      std::lock_guard<std::mutex> lk(g_park_mu);
+      g_parked.push_back(p);
+      p = nullptr;
+      n = 0;
+      return;
+    }
+    free();
   }
 };
 
@@ -379,6 +435,24 @@ void ensure_static(ttdvm_ctx* c) {
   }
 }
 
+// TTDVM_ARENA_LOG=1: report arena regrowth and overflow-repeat events (phase,
+// sizes, host time of the reallocation) on stderr.
+bool diag_log_on() {
+  static const bool on = [] {
+    const char* e = getenv("TTDVM_ARENA_LOG");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+void arena_log(ttdvm_ctx* c, const char* what, size_t from, size_t to,
+               std::chrono::steady_clock::time_point t0) {
+  if (!diag_log_on()) return;
+  const double ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  fprintf(stderr, "[ttdvm arena] phase %d %s: %.2f -> %.2f GB (%.1f ms)\n", c->cur_phase, what,
+          from * 8e-9, to * 8e-9, ms);
+}
+
 // Run one rounding launch: sets bound into RoundArgs, output into `out`.
 // Repeats the launch with a larger arena if it overflowed.
 void grow_preserve(ttdvm_ctx* c, TensorSet& s, long long keep, long long need);
@@ -538,8 +612,13 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     // path below nor the regrowth itself (a multi-GB cudaFree + cudaMalloc,
     // up to hundreds of ms) recurs step after step as the ranks creep up
     if ((double)out.arena.n < (double)out.used * 1.25 + 1024) {
-      out.arena.free();
+      const auto t0 = std::chrono::steady_clock::now();
+      const size_t was = out.arena.n;
+      out.arena.retire();
+      const auto t1 = std::chrono::steady_clock::now();
+      arena_log(c, "headroom regrow: release", was, 0, t0);
       out.arena.alloc((size_t)((double)out.used * 2.0) + 1024);
+      arena_log(c, "headroom regrow: cudaMalloc", was, out.arena.n, t1);
     }
   }
   for (int attempt = 0; attempt < 4; ++attempt) {
@@ -583,10 +662,30 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
           c->d_gscratch.alloc((size_t)grid * (size_t)a.gstride);
           a.gscratch = c->d_gscratch.p;
         }
+        const bool dlog = diag_log_on();
+        cudaEvent_t d0 = nullptr, d1 = nullptr;
+        if (dlog) {
+          CK(cudaEventCreate(&d0));
+          CK(cudaEventCreate(&d1));
+          CK(cudaEventRecord(d0, c->st));
+        }
         CK(l.wide     ? g256::launch_round_gram(a, grid, c->st)
            : l.narrow ? g32::launch_round_gram(a, grid, c->st)
                       : g128::launch_round_gram(a, grid, c->st));
         c->launches += 1;
+        if (dlog) {  // diagnostics only: per-bin device time (serialises the launches)
+          CK(cudaEventRecord(d1, c->st));
+          CK(cudaEventSynchronize(d1));
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, d0, d1);
+          cudaEventDestroy(d0);
+          cudaEventDestroy(d1);
+          fprintf(stderr,
+                  "[ttdvm bin] phase %d bin %d outputs %d summed ranks %dx%d D %d jb %d %s%s grid %d:"
+                  " %.2f ms\n",
+                  c->cur_phase, l.bin, l.count, l.rm1, l.rm2, gram_d(l.rm1, l.rm2), l.jb,
+                  l.wide ? "g256" : (l.narrow ? "g32" : "g128"), l.spill ? " spill" : "", grid, ms);
+        }
       }
     }
     CK(cudaMemcpyAsync(c->h_status, c->d_status.p, (kStWords + 4) * sizeof(int),
@@ -608,10 +707,12 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
         *reinterpret_cast<unsigned long long*>(c->h_status + kStWords);
     if (c->h_status[kStOverflow]) {
       const size_t want = std::max<size_t>(out.arena.n + 1024, (size_t)(used * 1.5) + 1024);
+      arena_log(c, "overflow, launch repeated", out.arena.n, want,
+                std::chrono::steady_clock::now());
       if (append) {
         grow_preserve(c, out, base_used, (long long)want);
       } else {
-        out.arena.free();
+        out.arena.retire();
         out.arena.alloc(want);
       }
       continue;
@@ -1130,7 +1231,7 @@ void grow_preserve(ttdvm_ctx* c, TensorSet& s, long long keep, long long need) {
   nb.alloc((size_t)std::max<long long>(need, (long long)(s.arena.n * 3 / 2)));
   if (keep > 0) CK(cudaMemcpyAsync(nb.p, s.arena.p, 8LL * keep, cudaMemcpyDeviceToDevice, c->st));
   CK(cudaStreamSynchronize(c->st));
-  s.arena.free();
+  s.arena.retire();
   s.arena = nb;
   nb.p = nullptr;
   nb.n = 0;
@@ -1378,6 +1479,7 @@ int ttdvm_cuda_destroy(ttdvm_ctx* c) {
   if (!c) return TTDVM_EINVAL;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
+  flush_parked();
   for (TensorSet* s : {&c->state[0], &c->state[1], &c->fsraw, &c->fs, &c->jr, &c->phi, &c->res,
                        &c->freestream, &c->in, &c->result, &c->xin, &c->eabs})
     s->free();

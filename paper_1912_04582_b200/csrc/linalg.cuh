@@ -118,6 +118,18 @@ __device__ __forceinline__ int floor_pow2(int x) {
   while (p * 2 <= x) p *= 2;
   return p;
 }
+// Jacobi stopping rule: stop after a sweep in which every coupling
+// gamma^2 / (alpha beta) stayed below TTDVM_JACOBI_BIG2.  By the quadratic
+// convergence of cyclic Jacobi the couplings left after that sweep are
+// O(TTDVM_JACOBI_BIG2).  The rounding kernels use 1e-10: the left-over
+// couplings (~1e-10 relative) perturb the kept singular values by ~1e-20
+// and the bases by ~1e-10, far below any rounding tolerance the step uses,
+// and about one sweep in 2.4 is saved (config-4 flux phase -3 %, same-box
+// A/B in scripts/gpu_ab_jacobi.sh).  facefactor.cu (from_full at 1e-12)
+// keeps 1e-18.
+#ifndef TTDVM_JACOBI_BIG2
+#define TTDVM_JACOBI_BIG2 1e-10
+#endif
 // One-sided (Hestenes) Jacobi on the columns of X (m x c, ld ldx) with
 // tracked squared column norms (one dot product per pair and round; the
 // norms are refreshed at every sweep).
@@ -159,7 +171,7 @@ __device__ int jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
         if (live && ga != 0.0) {
           const double al = nrm[a], be = nrm[b];
           if (ga * ga > tol2 * al * be) {
-            big = big || (ga * ga > 1e-18 * al * be);
+            big = big || (ga * ga > TTDVM_JACOBI_BIG2 * al * be);
             // t = sign(d) 2 ga / (|d| + sqrt(d^2 + 4 ga^2)), d = be - al: the
             // angle needs no more than FP32 accuracy (an inexact angle only
             // slows convergence); cs, sn are normalised in FP64 so the
@@ -551,7 +563,7 @@ __device__ int jacobi_warp_t(double* X, int ldx, int m, int c, double* nrm) {
         if (live && ga != 0.0) {
           const double al = nrm[a], be = nrm[b];
           if (ga * ga > tol2 * al * be) {
-            big = big || (ga * ga > 1e-18 * al * be);
+            big = big || (ga * ga > TTDVM_JACOBI_BIG2 * al * be);
             const double dlt = be - al;
             const double mag = fmax(fabs(dlt), 2.0 * fabs(ga));
             const int ex = (int)((__double_as_longlong(mag) >> 52) & 0x7ff) - 1023;
