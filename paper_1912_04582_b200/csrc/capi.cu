@@ -344,6 +344,9 @@ struct ttdvm_ctx {
   int cur_phase = 7;
   long long launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // auxiliary streams for concurrent rank bins (run_round), created lazily
+  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr, join_ev[3] = {nullptr, nullptr, nullptr};
 };
 
 namespace {
@@ -642,7 +645,45 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
       CK(launch_round(a, c->st));
       c->launches += 1;
     } else {
-      for (const Launch& l : plan) {
+      // Rank bins are independent launches (disjoint outputs; the arena bump
+      // counter, status words and FLOP accumulators are atomics).  The bin
+      // with the most outputs runs on the context stream; the other bins --
+      // a few hundred high-rank outputs each, whose single-CTA latency
+      // (2-10 ms) would otherwise leave most SMs idle -- run concurrently on
+      // auxiliary streams (spill bins serialised on aux[0]: they share the
+      // spill scratch).  TTDVM_BIN_STREAMS=0 serialises everything (A/B).
+      static const bool bin_streams = [] {
+        const char* e = getenv("TTDVM_BIN_STREAMS");
+        return !(e && *e == '0');
+      }();
+      const bool dlog = diag_log_on();
+      const bool fork = bin_streams && !dlog && plan.size() > 1;
+      size_t big = 0;
+      for (size_t i = 1; i < plan.size(); ++i)
+        if (plan[i].count > plan[big].count) big = i;
+      bool used_aux[3] = {false, false, false};
+      if (fork) {
+        if (!c->fork_ev) {
+          CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+          for (int k = 0; k < 3; ++k) {
+            CK(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->join_ev[k], cudaEventDisableTiming));
+          }
+        }
+        CK(cudaEventRecord(c->fork_ev, c->st));
+      }
+      int rr = 0;
+      for (size_t li = 0; li < plan.size(); ++li) {
+        const Launch& l = plan[li];
+        cudaStream_t lst = c->st;
+        if (fork && li != big) {
+          const int k = l.spill ? 0 : 1 + (rr++ & 1);
+          if (!used_aux[k]) {
+            CK(cudaStreamWaitEvent(c->aux[k], c->fork_ev, 0));
+            used_aux[k] = true;
+          }
+          lst = c->aux[k];
+        }
         a.RM1 = l.rm1;
         a.RM2 = l.rm2;
         a.MSMAX = l.ms;
@@ -662,16 +703,15 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
           c->d_gscratch.alloc((size_t)grid * (size_t)a.gstride);
           a.gscratch = c->d_gscratch.p;
         }
-        const bool dlog = diag_log_on();
         cudaEvent_t d0 = nullptr, d1 = nullptr;
         if (dlog) {
           CK(cudaEventCreate(&d0));
           CK(cudaEventCreate(&d1));
           CK(cudaEventRecord(d0, c->st));
         }
-        CK(l.wide     ? g256::launch_round_gram(a, grid, c->st)
-           : l.narrow ? g32::launch_round_gram(a, grid, c->st)
-                      : g128::launch_round_gram(a, grid, c->st));
+        CK(l.wide     ? g256::launch_round_gram(a, grid, lst)
+           : l.narrow ? g32::launch_round_gram(a, grid, lst)
+                      : g128::launch_round_gram(a, grid, lst));
         c->launches += 1;
         if (dlog) {  // diagnostics only: per-bin device time (serialises the launches)
           CK(cudaEventRecord(d1, c->st));
@@ -687,6 +727,11 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
                   l.wide ? "g256" : (l.narrow ? "g32" : "g128"), l.spill ? " spill" : "", grid, ms);
         }
       }
+      for (int k = 0; k < 3; ++k)
+        if (used_aux[k]) {
+          CK(cudaEventRecord(c->join_ev[k], c->aux[k]));
+          CK(cudaStreamWaitEvent(c->st, c->join_ev[k], 0));
+        }
     }
     CK(cudaMemcpyAsync(c->h_status, c->d_status.p, (kStWords + 4) * sizeof(int),
                        cudaMemcpyDeviceToHost, c->st));
@@ -1502,6 +1547,14 @@ int ttdvm_cuda_destroy(ttdvm_ctx* c) {
   if (c->h_status) cudaFreeHost(c->h_status);
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
+  if (c->fork_ev) {
+    for (int k = 0; k < 3; ++k) {
+      cudaStreamSynchronize(c->aux[k]);
+      cudaStreamDestroy(c->aux[k]);
+      cudaEventDestroy(c->join_ev[k]);
+    }
+    cudaEventDestroy(c->fork_ev);
+  }
   cudaStreamDestroy(c->st);
   delete c;
   return TTDVM_OK;
