@@ -135,6 +135,11 @@ struct Fail {
 // allocation fails (then retried once) and when a context is destroyed.  The
 // parked total stays below the live arenas' own size (each regrowth at least
 // doubles).  TTDVM_DEFER_FREE=0 restores immediate frees (A/B).
+// Blocks above kParkMaxBytes are freed at once and regrown without headroom:
+// the memory-tight configurations (config 5's blocked step runs within a few
+// GB of the 180 GB) must not carry parked or headroom copies of their large
+// arenas into the out-of-memory fallback.
+constexpr size_t kParkMaxBytes = 4ull << 30;
 std::mutex g_park_mu;
 std::vector<void*> g_parked;
 bool defer_free_on() {
@@ -168,7 +173,7 @@ struct DevBuf {
     const bool regrow = p != nullptr;
     retire();
     if (count == 0) return;
-    const size_t want = regrow ? count + count / 2 : count;
+    const size_t want = regrow && count * sizeof(T) <= kParkMaxBytes ? count + count / 2 : count;
     cudaError_t e = cudaMalloc(&p, want * sizeof(T));
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -194,7 +199,7 @@ struct DevBuf {
   // caller guarantees no pending work still reads the block's content
   // beyond the stream order (parked blocks are only freed after a device sync)
   void retire() {
-    if (p && defer_free_on()) {
+    if (p && defer_free_on() && n * sizeof(T) <= kParkMaxBytes) {
       std::lock_guard<std::mutex> lk(g_park_mu);
       g_parked.push_back(p);
       p = nullptr;
@@ -456,6 +461,22 @@ void arena_log(ttdvm_ctx* c, const char* what, size_t from, size_t to,
           from * 8e-9, to * 8e-9, ms);
 }
 
+// Arena size for a regrowth: `want` doubles when the device has room for
+// it (keeping 4 GB for the step's other buffers), else as much as fits but
+// at least `need` -- headroom must never turn a fitting step into an
+// out-of-memory failure (config 5 runs within a few GB of the 180 GB).
+size_t fit_free(size_t want, size_t need) {
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();
+    return want;
+  }
+  const size_t keep = 4ull << 30;
+  const size_t room = fr > keep ? (fr - keep) / sizeof(double) : 0;
+  if (want <= room) return want;
+  return std::max(need, room);
+}
+
 // Run one rounding launch: sets bound into RoundArgs, output into `out`.
 // Repeats the launch with a larger arena if it overflowed.
 void grow_preserve(ttdvm_ctx* c, TensorSet& s, long long keep, long long need);
@@ -620,7 +641,8 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
       out.arena.retire();
       const auto t1 = std::chrono::steady_clock::now();
       arena_log(c, "headroom regrow: release", was, 0, t0);
-      out.arena.alloc((size_t)((double)out.used * 2.0) + 1024);
+      out.arena.alloc(fit_free((size_t)((double)out.used * 2.0) + 1024,
+                               (size_t)((double)out.used * 1.05) + 1024));
       arena_log(c, "headroom regrow: cudaMalloc", was, out.arena.n, t1);
     }
   }
@@ -751,7 +773,8 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     const unsigned long long used =
         *reinterpret_cast<unsigned long long*>(c->h_status + kStWords);
     if (c->h_status[kStOverflow]) {
-      const size_t want = std::max<size_t>(out.arena.n + 1024, (size_t)(used * 1.5) + 1024);
+      const size_t want = fit_free(std::max<size_t>(out.arena.n + 1024, (size_t)(used * 1.5) + 1024),
+                                   std::max<size_t>(out.arena.n + 1024, (size_t)used + 1024));
       arena_log(c, "overflow, launch repeated", out.arena.n, want,
                 std::chrono::steady_clock::now());
       if (append) {
@@ -1487,12 +1510,29 @@ void download_set(ttdvm_ctx* c, const TensorSet& s, double* cores, int64_t capac
   const long long total = offs[s.count];
   require(capacity >= total, "download capacity too small: need " + std::to_string(total));
   if (s.count == 0) return;
+  // gathered in chunks of at most kChunk doubles (2 GB), so a download never
+  // needs a staging copy of the whole set next to the step's arenas (config
+  // 5's state is ~19 GB with the device nearly full); one chunk for config 4
+  constexpr long long kChunk = 256LL << 20;
   c->d_tmp_off.alloc(s.count);
-  c->d_tmp.alloc(std::max<long long>(1, total));
-  CK(cudaMemcpy(c->d_tmp_off.p, offs.data(), 8LL * s.count, cudaMemcpyHostToDevice));
-  CK(launch_gather(s.view(), s.count, c->d_tmp_off.p, c->n, c->n, c->n, c->d_tmp.p, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  CK(cudaMemcpy(cores, c->d_tmp.p, 8LL * total, cudaMemcpyDeviceToHost));
+  c->d_tmp.alloc((size_t)std::max<long long>(1, std::min(total, kChunk)));
+  int t0 = 0;
+  while (t0 < s.count) {
+    int t1 = t0 + 1;  // a single tensor always fits (<= n^3 r^2 doubles << kChunk)
+    while (t1 < s.count && offs[t1 + 1] - offs[t0] <= (long long)c->d_tmp.n) ++t1;
+    const long long base = offs[t0], len = offs[t1] - offs[t0];
+    std::vector<long long> rel(t1 - t0);
+    for (int t = t0; t < t1; ++t) rel[t - t0] = offs[t] - base;
+    CK(cudaMemcpy(c->d_tmp_off.p, rel.data(), 8LL * (t1 - t0), cudaMemcpyHostToDevice));
+    TSet v = s.view();
+    v.ranks += 2LL * t0;
+    v.off += t0;
+    if (v.tscale) v.tscale += t0;
+    CK(launch_gather(v, t1 - t0, c->d_tmp_off.p, c->n, c->n, c->n, c->d_tmp.p, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaMemcpy(cores + base, c->d_tmp.p, 8LL * len, cudaMemcpyDeviceToHost));
+    t0 = t1;
+  }
 }
 
 }  // namespace
