@@ -1513,7 +1513,11 @@ void download_set(ttdvm_ctx* c, const TensorSet& s, double* cores, int64_t capac
   // gathered in chunks of at most kChunk doubles (2 GB), so a download never
   // needs a staging copy of the whole set next to the step's arenas (config
   // 5's state is ~19 GB with the device nearly full); one chunk for config 4
-  constexpr long long kChunk = 256LL << 20;
+  long long kChunk = 256LL << 20;
+  if (const char* e = getenv("TTDVM_DOWNLOAD_CHUNK")) {  // tests: force many chunks
+    const long long v = atoll(e);
+    if (v > 0) kChunk = v;
+  }
   c->d_tmp_off.alloc(s.count);
   c->d_tmp.alloc((size_t)std::max<long long>(1, std::min(total, kChunk)));
   int t0 = 0;

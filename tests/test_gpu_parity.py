@@ -318,6 +318,22 @@ def test_step_many_steps_stable(ctx):
     assert np.all(m[:, 0] > 0) and np.all(m[:, 4] > 0)
 
 
+def test_download_in_chunks_matches_one_gather(ctx, monkeypatch):
+    """The state download gathers in bounded chunks (capi.cu download_set,
+    2 GB by default so config 5's 19 GB state needs no full staging copy):
+    forcing chunks of a few tensors gives bitwise the one-chunk result."""
+    p = config(1)
+    ctx.setup(p)
+    ctx.step(p.dt, p.eps, p.cap, 3)
+    whole = ctx.download_state()
+    sizes = np.diff(whole.offsets)
+    monkeypatch.setenv("TTDVM_DOWNLOAD_CHUNK", str(int(3 * sizes.max())))
+    parts = ctx.download_state()
+    monkeypatch.delenv("TTDVM_DOWNLOAD_CHUNK")
+    assert np.array_equal(parts.ranks, whole.ranks)
+    assert np.array_equal(parts.cores, whole.cores)
+
+
 def test_partitioned_step_two_contexts():
     """Two library contexts on one GPU, each owning an x-slab of a periodic
     box with ghost cells, stepped one after the other with halo pack/unpack
