@@ -1510,19 +1510,21 @@ void download_set(ttdvm_ctx* c, const TensorSet& s, double* cores, int64_t capac
   const long long total = offs[s.count];
   require(capacity >= total, "download capacity too small: need " + std::to_string(total));
   if (s.count == 0) return;
-  // gathered in chunks of at most kChunk doubles (2 GB), so a download never
+  // gathered in chunks of at most `chunk` doubles (2 GB), so a download never
   // needs a staging copy of the whole set next to the step's arenas (config
   // 5's state is ~19 GB with the device nearly full); one chunk for config 4
-  long long kChunk = 256LL << 20;
+  long long chunk = 256LL << 20;
   if (const char* e = getenv("TTDVM_DOWNLOAD_CHUNK")) {  // tests: force many chunks
     const long long v = atoll(e);
-    if (v > 0) kChunk = v;
+    if (v > 0) chunk = v;
   }
   c->d_tmp_off.alloc(s.count);
-  c->d_tmp.alloc((size_t)std::max<long long>(1, std::min(total, kChunk)));
+  long long maxsz = 1;
+  for (int t = 0; t < s.count; ++t) maxsz = std::max<long long>(maxsz, offs[t + 1] - offs[t]);
+  c->d_tmp.alloc((size_t)std::max(maxsz, std::min(total, chunk)));
   int t0 = 0;
   while (t0 < s.count) {
-    int t1 = t0 + 1;  // a single tensor always fits (<= n^3 r^2 doubles << kChunk)
+    int t1 = t0 + 1;  // one tensor per chunk at least
     while (t1 < s.count && offs[t1 + 1] - offs[t0] <= (long long)c->d_tmp.n) ++t1;
     const long long base = offs[t0], len = offs[t1] - offs[t0];
     std::vector<long long> rel(t1 - t0);
