@@ -472,7 +472,11 @@ size_t fit_free(size_t want, size_t need) {
     return want;
   }
   const size_t keep = 4ull << 30;
-  const size_t room = fr > keep ? (fr - keep) / sizeof(double) : 0;
+  size_t room = fr > keep ? (fr - keep) / sizeof(double) : 0;
+  // parked blocks (DevBuf::retire) are not counted free by cudaMemGetInfo:
+  // release them before clamping a regrowth below its wish
+  if (want > room && flush_parked() && cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+    room = fr > keep ? (fr - keep) / sizeof(double) : 0;
   if (want <= room) return want;
   return std::max(need, room);
 }
@@ -642,7 +646,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
       const auto t1 = std::chrono::steady_clock::now();
       arena_log(c, "headroom regrow: release", was, 0, t0);
       out.arena.alloc(fit_free((size_t)((double)out.used * 2.0) + 1024,
-                               (size_t)((double)out.used * 1.05) + 1024));
+                               std::max(was, (size_t)out.used + 1024)));
       arena_log(c, "headroom regrow: cudaMalloc", was, out.arena.n, t1);
     }
   }
@@ -680,9 +684,31 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
       }();
       const bool dlog = diag_log_on();
       const bool fork = bin_streams && !dlog && plan.size() > 1;
+      // Spill bins share one scratch buffer (d_gscratch), so they all run on
+      // one stream: the context stream when the biggest bin spills, aux[0]
+      // otherwise.  The scratch is sized once for the largest spill launch
+      // before any launch is issued (a regrowth between launches would free
+      // a block a queued launch still uses).
       size_t big = 0;
       for (size_t i = 1; i < plan.size(); ++i)
         if (plan[i].count > plan[big].count) big = i;
+      const bool big_spills = !plan.empty() && plan[big].spill;
+      size_t scratch_need = 0;
+      for (const Launch& l : plan) {
+        if (!l.spill) continue;
+        int resident = 0;
+        RoundArgs ra = a;
+        ra.RM1 = l.rm1;
+        ra.RM2 = l.rm2;
+        ra.MSMAX = l.ms;
+        ra.JB = l.jb;
+        CK(l.wide ? g256::round_gram_resident(ra, &resident)
+                  : g128::round_gram_resident(ra, &resident));
+        if (resident <= 0) throw Fail{TTDVM_ENOMEM, "spill rounding plan does not fit an SM"};
+        const size_t g = (size_t)std::min(l.count, resident);
+        scratch_need = std::max(scratch_need, g * (size_t)round_gram_spill_doubles(n, n, l.rm1, l.rm2));
+      }
+      if (scratch_need) c->d_gscratch.alloc(scratch_need);
       bool used_aux[3] = {false, false, false};
       if (fork) {
         if (!c->fork_ev) {
@@ -698,7 +724,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
       for (size_t li = 0; li < plan.size(); ++li) {
         const Launch& l = plan[li];
         cudaStream_t lst = c->st;
-        if (fork && li != big) {
+        if (fork && li != big && !(l.spill && big_spills)) {
           const int k = l.spill ? 0 : 1 + (rr++ & 1);
           if (!used_aux[k]) {
             CK(cudaStreamWaitEvent(c->aux[k], c->fork_ev, 0));
@@ -722,7 +748,8 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
           if (resident <= 0) throw Fail{TTDVM_ENOMEM, "spill rounding plan does not fit an SM"};
           grid = std::min(l.count, resident);
           a.gstride = round_gram_spill_doubles(n, n, l.rm1, l.rm2);
-          c->d_gscratch.alloc((size_t)grid * (size_t)a.gstride);
+          if ((size_t)grid * (size_t)a.gstride > c->d_gscratch.n)
+            throw Fail{TTDVM_ENOMEM, "spill scratch smaller than planned"};
           a.gscratch = c->d_gscratch.p;
         }
         cudaEvent_t d0 = nullptr, d1 = nullptr;
@@ -1296,7 +1323,14 @@ void build_step_terms(ttdvm_ctx* c) {
 void grow_preserve(ttdvm_ctx* c, TensorSet& s, long long keep, long long need) {
   if ((long long)s.arena.n >= need) return;
   DevBuf<double> nb;
-  nb.alloc((size_t)std::max<long long>(need, (long long)(s.arena.n * 3 / 2)));
+  // The old arena is still held during the copy, so large arenas (config 5's
+  // blocked step runs within a few GB of the 180 GB) grow exactly; small ones
+  // take 1.5x headroom, clamped to the free device memory.
+  const size_t exact = (size_t)need;
+  const size_t want = exact * sizeof(double) > kParkMaxBytes
+                          ? exact
+                          : fit_free(std::max(exact, s.arena.n * 3 / 2), exact);
+  nb.alloc(want);
   if (keep > 0) CK(cudaMemcpyAsync(nb.p, s.arena.p, 8LL * keep, cudaMemcpyDeviceToDevice, c->st));
   CK(cudaStreamSynchronize(c->st));
   s.arena.retire();
@@ -1521,11 +1555,14 @@ void download_set(ttdvm_ctx* c, const TensorSet& s, double* cores, int64_t capac
   c->d_tmp_off.alloc(s.count);
   long long maxsz = 1;
   for (int t = 0; t < s.count; ++t) maxsz = std::max<long long>(maxsz, offs[t + 1] - offs[t]);
-  c->d_tmp.alloc((size_t)std::max(maxsz, std::min(total, chunk)));
+  const long long lim = std::max(maxsz, std::min(total, chunk));
+  c->d_tmp.alloc((size_t)lim);
   int t0 = 0;
   while (t0 < s.count) {
+    // chunks are bounded by the requested chunk size, not by the staging
+    // buffer (which never shrinks and may hold a whole earlier download)
     int t1 = t0 + 1;  // one tensor per chunk at least
-    while (t1 < s.count && offs[t1 + 1] - offs[t0] <= (long long)c->d_tmp.n) ++t1;
+    while (t1 < s.count && offs[t1 + 1] - offs[t0] <= lim) ++t1;
     const long long base = offs[t0], len = offs[t1] - offs[t0];
     std::vector<long long> rel(t1 - t0);
     for (int t = t0; t < t1; ++t) rel[t - t0] = offs[t] - base;
@@ -1535,6 +1572,7 @@ void download_set(ttdvm_ctx* c, const TensorSet& s, double* cores, int64_t capac
     v.off += t0;
     if (v.tscale) v.tscale += t0;
     CK(launch_gather(v, t1 - t0, c->d_tmp_off.p, c->n, c->n, c->n, c->d_tmp.p, c->st));
+    c->launches += 1;
     CK(cudaStreamSynchronize(c->st));
     CK(cudaMemcpy(cores + base, c->d_tmp.p, 8LL * len, cudaMemcpyDeviceToHost));
     t0 = t1;
@@ -1575,6 +1613,9 @@ int ttdvm_cuda_destroy(ttdvm_ctx* c) {
                        &c->freestream, &c->in, &c->result, &c->xin, &c->eabs})
     s->free();
   for (TermList* t : {&c->t_fs, &c->t_col, &c->t_flux, &c->t_res, &c->t_upd, &c->t_batch}) t->free();
+  for (auto* v : {&c->bt_flux, &c->bt_res, &c->bt_upd})
+    for (TermList& t : *v) t.free();
+  c->d_gscratch.free();
   c->d_nodes.free();
   c->d_weights.free();
   c->d_factors.free();

@@ -328,8 +328,12 @@ def test_download_in_chunks_matches_one_gather(ctx, monkeypatch):
     whole = ctx.download_state()
     sizes = np.diff(whole.offsets)
     monkeypatch.setenv("TTDVM_DOWNLOAD_CHUNK", str(int(3 * sizes.max())))
+    l0 = ctx.launch_count()
     parts = ctx.download_state()
+    gathers = ctx.launch_count() - l0
     monkeypatch.delenv("TTDVM_DOWNLOAD_CHUNK")
+    # chunks of <= 3 of the largest tensors: at least total / (3 max) gathers
+    assert gathers >= max(2, math.ceil(whole.offsets[-1] / (3 * sizes.max()))), gathers
     assert np.array_equal(parts.ranks, whole.ranks)
     assert np.array_equal(parts.cores, whole.cores)
 
