@@ -129,10 +129,9 @@ def test_step_obstacle_lockstep(ctx):
     (every interior face oblique, diffuse walls, free-stream in/out)."""
     from test_gpu_parity import check_step
     p = small_obstacle(nv=12)
-    worst, flips = check_step(ctx, p, 3)
+    check_step(ctx, p, 3)  # every rank mismatch margin-checked inside
     info = ctx.setup_info()
     assert info["oblique_normals"] > 0 and info["wall_faces"] > 0
-    assert flips <= 2, (worst, flips)
 
 
 def test_step_obstacle_stages(ctx):
