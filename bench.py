@@ -45,12 +45,15 @@ import numpy as np  # noqa: E402
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=0,
+                    help="0 = the config's own step count (20 for config 4, 10 for config 5)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the sampled oracle lock-step check after the timed region")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     return ap.parse_args()
 
@@ -137,59 +140,91 @@ def _one_blas_thread():
         pass
 
 
-def _ref_worker_init(args_tuple):
-    """Per worker: the problem, an oracle solver, and its face-factor cache
-    filled for every face of ``warm_cells`` -- the one-time set-up the GPU
-    arm also keeps out of its timed steps (pool.map hands a strip to
-    whichever worker is free, so every worker warms every strip)."""
-    _one_blas_thread()
-    global _W
-    cfg, scale, warm_cells = args_tuple
-    from oracle.step import OracleSolver
-    from oracle.tt import TtTensor
-    from paper_1912_04582_b200.problems import config
-    p = config(cfg, scale)
-    solver = OracleSolver(p.mesh, p.nv, p.bound, p.gas, p.bcs)
-    for c in warm_cells:
-        for fid, _ in p.mesh.cell_faces(c):
-            solver.factors(p.mesh.face_normal[fid])
-    _W = (p, solver, TtTensor)
+def ref_sample_part(p, nblocks: int, b: int, seed: int = 7):
+    """A bounded sample of the workload for the CPU arms: ``nblocks``
+    contiguous b^3 blocks of cells at seeded uniform positions of the mesh
+    lattice, as one local mesh (partition.build_part) with a one-cell ghost
+    ring around every block.  Interior faces are shared by two sampled cells,
+    so the flux work per cell is amortised as in the full step (b = 6:
+    3.5 faces per cell against the mesh's 3.04); the ghost ring stays frozen
+    at the initial state.  Returns None when the mesh is no larger than the
+    sample (the whole mesh is stepped then)."""
+    from paper_1912_04582_b200.partition import build_part
+    m = p.mesh
+    if m.cell_ijk is None or m.ncell <= nblocks * b ** 3:
+        return None
+    rng = np.random.default_rng(seed)
+    ijk = m.cell_ijk
+    mask = np.zeros(m.ncell, dtype=bool)
+    for _ in range(nblocks):
+        o = np.array([int(rng.integers(0, max(1, sdim - b + 1))) for sdim in m.shape])
+        mask |= np.all((ijk >= o[None, :]) & (ijk < (o + b)[None, :]), axis=1)
+    return build_part(m, np.where(mask, 0, 1).astype(np.int32), 0)
 
 
-def _ref_task(cells):
-    p, solver, TtTensor = _W
-    need = set(cells)
-    for c in cells:
-        for fid, _ in p.mesh.cell_faces(c):
-            need.add(int(p.mesh.face_left[fid]))
-            r = int(p.mesh.face_right[fid])
-            if r >= 0:
-                need.add(r)
-    f = {i: TtTensor(*p.f0.get(i)) for i in need}
-    t = time.perf_counter()
-    solver.step(f, p.dt, p.eps, p.cap, cells=list(cells))
-    return time.perf_counter() - t
-
-
-def cpu_oracle_rate(cfg, scale, ncells: int, workers: int, repeats: int = 1):
-    """Cell-steps/s of the oracle on a sample of the workload's cells: each
-    worker steps a strip of `ncells` consecutive cells (with the fluxes of
-    every face they touch) from the workload's initial state."""
-    import multiprocessing as mp
-    from paper_1912_04582_b200.problems import config
-    p = config(cfg, scale)
-    strips = [list(range(w * ncells, (w + 1) * ncells)) for w in range(workers)]
-    strips = [[c % p.mesh.ncell for c in s] for s in strips]
-    ctxm = mp.get_context("spawn")
-    times = []
-    warm = sorted({c for st in strips for c in st})
-    with ctxm.Pool(workers, initializer=_ref_worker_init, initargs=((cfg, scale, warm),)) as pool:
-        pool.map(_ref_task, strips)  # warm: imports and the strips' face factors
-        for _ in range(repeats):
+def cpu_reference_rate(p, nblocks: int, b: int, warmup: int, steps: int, threads: int):
+    """Cell-steps/s of the reference CPU implementation on a bounded sample
+    (ref_sample_part), advanced through warmup + steps explicit steps from
+    the workload's initial state -- so its ranks grow with the step number
+    as the GPU arm's do.  The compiled reference (oracle/_ref: the unmodified
+    proj/src/*.cpp, S1 composed of reference calls, OpenMP over faces and
+    cells) when its library is present, else the numpy port.  One-time
+    face-factor set-up is kept out of the timed steps, as in the GPU arm.
+    Returns (rate, info dict)."""
+    from oracle import ref
+    from paper_1912_04582_b200.partition import local_state
+    part = ref_sample_part(p, nblocks, b)
+    mesh = p.mesh if part is None else part.mesh
+    f0 = p.f0 if part is None else local_state(part, p.f0)
+    nown = p.mesh.ncell if part is None else part.n_owned
+    cells = np.arange(nown, dtype=np.int32)
+    t_setup = time.perf_counter()
+    if ref.available():
+        kind = "reference"
+        r = ref.RefSolver(p.nv, p.bound, p.gas, mesh, p.bcs, threads=threads)
+        r.set_state(f0)
+        r.step(p.dt, p.eps, p.cap, cells=cells)   # fills the face-factor cache (one-time)
+        r.set_state(f0)
+        setup_s = time.perf_counter() - t_setup
+        for _ in range(warmup):
+            r.step(p.dt, p.eps, p.cap, cells=cells)
+        t = time.perf_counter()
+        for _ in range(steps):
+            r.step(p.dt, p.eps, p.cap, cells=cells)
+        el = time.perf_counter() - t
+        max_rank = int(r.state().ranks[:nown].max())
+        r.close()
+        what = "compiled reference C++ (oracle/_ref, OpenMP)"
+    else:
+        kind, threads = "port", 1
+        _one_blas_thread()
+        from oracle.parity import oracle_list
+        from oracle.step import OracleSolver
+        solver = OracleSolver(mesh, p.nv, p.bound, p.gas, p.bcs)
+        f = dict(enumerate(oracle_list(f0)))
+        for c in cells:
+            for fid, _ in mesh.cell_faces(int(c)):
+                solver.factors(mesh.face_normal[fid])
+        setup_s = time.perf_counter() - t_setup
+        el = 0.0
+        for it in range(warmup + steps):
             t = time.perf_counter()
-            pool.map(_ref_task, strips)
-            times.append(time.perf_counter() - t)
-    return workers * ncells / min(times), times
+            out, _ = solver.step(f, p.dt, p.eps, p.cap, cells=[int(c) for c in cells])
+            if it >= warmup:
+                el += time.perf_counter() - t
+            for c, x in zip(cells, out):
+                f[int(c)] = x
+        max_rank = max(max(f[int(c)].ranks()) for c in cells)
+        what = "numpy port (oracle/step.py), 1 BLAS thread"
+    rate = nown * steps / el
+    info = {"kind": kind, "cores": threads, "cells": int(nown), "setup_s": round(setup_s, 1),
+            "max_rank_after": max_rank, "ms_per_step": 1e3 * el / steps,
+            "sample": (f"{nown} cells " + ("(the whole mesh)" if part is None else
+                       f"= {nblocks} contiguous {b}^3 blocks at seeded lattice positions, frozen "
+                       "one-cell ghost ring") + f", advanced through {warmup}+{steps} steps from "
+                       f"the initial state, {what}, {threads} threads, face factors set up before "
+                       "timing")}
+    return rate, info
 
 
 def run_reference(args):
@@ -198,36 +233,101 @@ def run_reference(args):
         return
     from paper_1912_04582_b200.problems import config
     p = config(args.config, args.scale)
-    workers = os.cpu_count() or 1
-    per = 2
-    import multiprocessing as mp
-    from paper_1912_04582_b200.problems import config as _c  # noqa: F401
-    strips = [[(w * per + k) % p.mesh.ncell for k in range(per)] for w in range(workers)]
-    ctxm = mp.get_context("spawn")
-    warm = sorted({c for st in strips for c in st})
-    with ctxm.Pool(workers, initializer=_ref_worker_init,
-                   initargs=((args.config, args.scale, warm),)) as pool:
-        pool.map(_ref_task, [[0]] * workers)
-        for _ in range(args.warmup):
-            pool.map(_ref_task, strips)
-        t = time.perf_counter()
-        for _ in range(args.steps):
-            pool.map(_ref_task, strips)
-        el = time.perf_counter() - t
-    value = workers * per * args.steps / el
+    threads = os.cpu_count() or 1
+    # ~8 blocks of 6^3 cells: ~6k distinct oblique normals of one-time
+    # face-factor set-up (~1 min on 16 cores), seconds of timed steps
+    nblocks = int(os.environ.get("TTDVM_REF_BLOCKS", "8"))
+    value, info = cpu_reference_rate(p, nblocks, 6, args.warmup, args.steps, threads)
     line = {"impl": "reference", "metric": "cell-steps/s", "value": value, "unit": "cell-steps/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": info["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(p, args),
-            "cpu_baseline": {"value": value, "unit": "cell-steps/s", "cores": workers,
-                             "kind": "port",
-                             "sample": f"{workers} processes x {per} cells of the workload per "
-                                       "step (faces they touch included), numpy oracle, 1 BLAS "
-                                       "thread each, face factors set up before timing"},
+            "cpu_baseline": {"value": value, "unit": "cell-steps/s", "cores": info["cores"],
+                             "kind": info["kind"], "sample": info["sample"],
+                             "setup_s": info["setup_s"], "max_rank_after": info["max_rank_after"]},
             "e2e": {"value": value, "unit": "cell-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ parity block
+def parity_block(p, st_prev, st_new, macros_prev, from_step: int, ncells: int = 64, seed: int = 0):
+    """Sampled full-size lock-step check of the run just timed: ``ncells``
+    cells of the workload -- half of them the highest-rank cells of the new
+    state and wall-adjacent cells (the disturbed region), half uniform --
+    are stepped by the oracle from the GPU's own state t^(K-1), with the
+    faces they touch and the neighbour states behind them, and compared with
+    the GPU's state t^K: per-cell reconstruction error (bar 10 eps),
+    macroparameters (1e-8), ranks (every mismatch inside the TIE window of an
+    oracle decision on the cell's chain, oracle/parity.py).  The oracle is
+    the checker here, never the thing measured."""
+    from oracle import parity, ref
+    from oracle.tt import rel_err
+    from paper_1912_04582_b200.partition import build_part
+    m = p.mesh
+    rng = np.random.default_rng(seed)
+    if not ref.available():
+        ncells = min(ncells, 8)  # the numpy port's face factors cost ~1 s per normal
+    ncells = min(ncells, m.ncell)
+    hot = []
+    walls = [g for g, bc in enumerate(p.bcs) if bc["kind"] == "wall"]
+    if walls:
+        wf = np.nonzero((m.face_right < 0) & np.isin(m.face_group, walls))[0]
+        hot = list(np.unique(m.face_left[wf])[:: max(1, len(wf) // max(1, ncells // 8))][:ncells // 8])
+    order = np.argsort(-st_new.ranks.max(1).astype(np.int64), kind="stable")
+    for c in order:
+        if len(hot) >= ncells // 2:
+            break
+        if int(c) not in hot:
+            hot.append(int(c))
+    rest = np.setdiff1d(np.arange(m.ncell), np.array(hot, dtype=np.int64))
+    cells = np.sort(np.concatenate([np.array(hot, dtype=np.int64),
+                                    rng.choice(rest, ncells - len(hot), replace=False)]))
+    owner = np.ones(m.ncell, dtype=np.int32)
+    owner[cells] = 0
+    part = build_part(m, owner, 0)
+    loc = st_prev.subset(part.local_to_global)
+    nown = part.n_owned
+    t0 = time.perf_counter()
+    if ref.available():
+        name = "compiled reference (oracle/_ref: unmodified proj/src/*.cpp, S1 of reference calls)"
+        r = ref.RefSolver(p.nv, p.bound, p.gas, part.mesh, p.bcs)
+        r.set_state(loc)
+        r.step(p.dt, p.eps, p.cap, cells=np.arange(nown, dtype=np.int32))
+        want = r.state()
+        wm = r.macros(nown)
+        r.close()
+    else:
+        name = "numpy port (oracle/step.py)"
+        from oracle.step import OracleSolver
+        from paper_1912_04582_b200.tt_batch import TtBatch
+        s = OracleSolver(part.mesh, p.nv, p.bound, p.gas, p.bcs)
+        out, mo = s.step(dict(enumerate(parity.oracle_list(loc))), p.dt, p.eps, p.cap,
+                         cells=list(range(nown)))
+        want = TtBatch.from_list(out)
+        wm = np.stack([x.as_array() for x in mo])
+    worst, flips = 0.0, []
+    for k in range(nown):
+        g = int(part.owned[k])
+        worst = max(worst, rel_err(st_new.full(g), want.full(k)))
+        if tuple(st_new.ranks[g]) != tuple(want.ranks[k]):
+            flips.append(k)
+    macro = parity.macro_err(macros_prev[part.owned], wm)
+    worst_margin = 0.0
+    if flips:
+        from oracle.step import OracleSolver
+        s = OracleSolver(part.mesh, p.nv, p.bound, p.gas, p.bcs)
+        cm = parity.ChainMargins(s, dict(enumerate(parity.oracle_list(loc))), p.dt, p.eps, p.cap)
+        worst_margin = max(min(cm.cell(k).values()) for k in flips)
+    tie = parity.tie(p.eps)
+    return {"cells": int(nown), "from_step": int(from_step), "oracle": name,
+            "max_rel_err": worst, "tol_rel_err": 10 * p.eps, "macro_max_rel": macro,
+            "tol_macro": 1e-8, "rank_flips": len(flips), "max_flip_margin": worst_margin,
+            "tie": tie, "max_rank_in_sample": int(want.ranks[:nown].max()),
+            "wall_adjacent_cells": int(len(walls) and min(len(hot), ncells // 8)),
+            "oracle_s": round(time.perf_counter() - t0, 1),
+            "pass": bool(worst <= 10 * p.eps and macro <= 1e-8 and worst_margin < tie)}
 
 
 # ------------------------------------------------- config 3: batched rounding
@@ -405,10 +505,58 @@ def run_config3(args):
 
 
 # ------------------------------------------------------------------- GPU arm
+def spawn_ranks(args):
+    """`python bench.py --gpus N` without torchrun: launch the N ranks here
+    (one process per GPU over NCCL) and fail loudly when fewer GPUs are visible."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible",
+              file=sys.stderr)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
+def kernel_rooflines(rep, steps, fp64_peak, hbm_peak):
+    """Per-kernel achieved rates of one profiled pass: algorithmic FLOPs and
+    bytes (ttdvm_cuda_phase_report) over the phase's device time, against
+    the measured DFMA peak and the measured HBM bandwidth."""
+    kernels = {"moments": ("macro_kernel", "hbm"), "shakhov_build": ("shakhov_raw_kernel", "hbm"),
+               "wall_densities": ("wall_kernel", "latency"),
+               "round_fs": ("round_gram_kernel<g32> (f_S)", "fp64"),
+               "round_collision": ("round_gram_kernel<g32> (f_S - f)", "fp64"),
+               "round_flux": ("round_gram_kernel (face fluxes)", "fp64"),
+               "round_residual": ("round_gram_kernel (cell residuals)", "fp64"),
+               "round_update": ("round_gram_kernel (f + dt R)", "fp64")}
+    out = {}
+    for name, (kern, bound) in kernels.items():
+        ms, fl, by, la = rep[name]
+        if ms <= 0.0 or la <= 0:
+            continue
+        tf, gbs = fl / ms / 1e9, by / ms / 1e6
+        out[name] = {"kernel": kern, "bound": bound, "ms_per_step": round(ms / steps, 4),
+                     "launches_per_step": round(la / steps, 2),
+                     "tflops": round(tf, 4), "fp64_frac": round(tf / fp64_peak, 5) if fp64_peak else None,
+                     "gbs": round(gbs, 2), "hbm_frac": round(gbs / hbm_peak, 5)}
+    return out
+
+
 def main():
     args = parse()
+    if args.steps <= 0:  # each config's own step count (BASELINE.json configs)
+        args.steps = {1: 100, 2: 50, 3: 5, 4: 20, 5: 10}.get(args.config, 5)
     if args.e2e_steps <= 0:
         args.e2e_steps = args.steps
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        spawn_ranks(args)
     if args.config == 3:
         run_config3(args)
         return
@@ -418,6 +566,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     import torch
     torch.cuda.set_device(local)
     dist = None
@@ -459,7 +610,7 @@ def main():
         ctx.set_owned(part.n_owned)
         f_local = local_state(part, pg.f0)
         ctx.upload_state(f_local)
-        pack, unpack = halo.gpu_pack_unpack(ctx, torch.device("cuda", local))
+        hx = halo.HaloExchange(ctx, part, torch.device("cuda", local))
         p = pg
         cells_per_rank = part.n_owned
     else:
@@ -471,8 +622,10 @@ def main():
     setup["face_factors_s"] = round(time.perf_counter() - t0, 2)
     setup.update({k: v for k, v in ctx.setup_info().items() if k != "face_factor_ms"})
     fp64_peak = ctx.fp64_peak()
+    hbm_peak = load_peaks().get("hbm_gbs", 6547.8)
 
     def run_steps(k):
+        """k steps; device ms by CUDA events on the stream the kernels run on."""
         if part is None:
             return ctx.timed_step(p.dt, p.eps, p.cap, k)
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -481,38 +634,31 @@ def main():
         ev0.record()
         for _ in range(k):
             ctx.step(p.dt, p.eps, p.cap, 1)
-            halo.exchange(part, pack, unpack, p.nv, device=torch.device("cuda", local))
+            hx.exchange()
         ev1.record()
         torch.cuda.synchronize()
         return ev0.elapsed_time(ev1)
 
+    # ---- timed region: steps 1..K from the initial state, profiling OFF ----
     run_steps(args.warmup)
-    ctx.upload_state(f_local)  # time steps 1..K from the initial state
-    ctx.set_profiling(True)
+    ctx.upload_state(f_local)
+    ctx.set_profiling(False)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ms = run_steps(args.steps)
     torch.cuda.synchronize()
-    phase_ms = ctx.phase_times()
-    flops, bytes_, launches = ctx.phase_work()
-    gpu_launches = ctx.launch_count()
+    gpu_launches = ctx.launch_count() * (1 if part is None else args.steps)
     setup["cell_blocks"] = ctx.setup_info()["cell_blocks"]  # grown on out-of-memory
-    st = ctx.download_state()
-    max_rank = int(st.ranks.max())
     if dist:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = ncell_total * args.steps / (ms / 1e3)
 
-    # e2e through the public API with host buffers: upload state, one step,
-    # download state -- every step
-    ctx.set_profiling(False)
-    # (the host state advances: steps 1..E from the initial state, as timed)
-    # pinned host buffer for the state's cores (the ranks / offsets arrays
-    # are small); the initial state is copied in before the timed region
+    # ---- e2e through the public API with host buffers: upload state, one
+    # step, download state -- every step (steps 1..E from the initial state)
     from paper_1912_04582_b200.tt_batch import TtBatch
     pinned = torch.empty(max(2 * f_local.cores.size, 1 << 20), dtype=torch.float64,
                          pin_memory=True).numpy()
@@ -521,6 +667,7 @@ def main():
                    pinned[:f_local.cores.size])
     if dist:
         dist.barrier()
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     h2d = d2h = 0
     for _ in range(args.e2e_steps):
@@ -528,7 +675,7 @@ def main():
         ctx.upload_state(host)
         ctx.step(p.dt, p.eps, p.cap, 1)
         if part is not None:
-            halo.exchange(part, pack, unpack, p.nv, device=torch.device("cuda", local))
+            hx.exchange()
         host = ctx.download_state(out=pinned)
         d2h += int(host.cores.nbytes + host.ranks.nbytes + host.offsets.nbytes)
     h2d //= args.e2e_steps
@@ -540,39 +687,79 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = ncell_total * args.e2e_steps / e2e_s
+    max_rank = int(host.ranks.max())
+    del host
 
-    # roofline of the dominant kernel (the rounding phase with most time)
-    names = ["moments", "shakhov_build", "round_fs", "round_collision", "round_flux",
-             "round_residual", "round_update", "bookkeeping"]
-    dom = int(np.argmax(phase_ms[2:7])) + 2
-    dom_s = phase_ms[dom] / 1e3
-    achieved = flops[dom] / dom_s / 1e12 if dom_s > 0 else 0.0
+    # ---- separate profiled pass over the same steps 1..K (per-phase CUDA
+    # events cost a sync per phase, so they stay out of the timed region);
+    # it also leaves the states t^(K-1) and t^K for the parity block
+    ctx.upload_state(f_local)
+    ctx.set_profiling(True)
+    rep = None
+    st_prev = st_new = macros_prev = None
+    for chunk in (args.steps - 1, 1):
+        if chunk <= 0:
+            continue
+        if part is None:
+            ctx.timed_step(p.dt, p.eps, p.cap, chunk)
+            r = ctx.phase_report()
+            rep = r if rep is None else {k: tuple(a + b for a, b in zip(rep[k], r[k])) for k in r}
+            if chunk == args.steps - 1:
+                st_prev = ctx.download_state()
+        else:
+            for _ in range(chunk):
+                ctx.timed_step(p.dt, p.eps, p.cap, 1)
+                r = ctx.phase_report()
+                rep = r if rep is None else {k: tuple(a + b for a, b in zip(rep[k], r[k]))
+                                             for k in r}
+                hx.exchange()
+    ctx.set_profiling(False)
+    parity = None
+    if part is None and rank == 0 and not args.no_parity:
+        if st_prev is None:
+            st_prev = f_local
+        st_new = ctx.download_state()
+        macros_prev = ctx.macros()
+        try:
+            parity = parity_block(p, st_prev, st_new, macros_prev, args.steps - 1)
+        except Exception as e:  # the bench line still prints; the failure is visible
+            parity = {"error": f"{type(e).__name__}: {e}", "pass": False}
+        del st_prev, st_new
+
+    # ---- rooflines: every kernel of the step, then the dominant one
+    per_kernel = kernel_rooflines(rep, args.steps, fp64_peak, hbm_peak)
+    rounds = [k for k in per_kernel if k.startswith("round_")]
+    dom = max(rounds, key=lambda k: per_kernel[k]["ms_per_step"])
+    d_ms, d_fl, d_by, d_la = rep[dom]
     # ncu DRAM bytes per rounded output of this phase (profiles/traffic.json),
     # times the phase's outputs per launch in this run
-    per_out = traffic_from_profiles().get(names[dom] + "_bytes_per_output")
+    per_out = traffic_from_profiles().get(dom + "_bytes_per_output")
     nface_local = (part.mesh if part is not None else p.mesh).nface
-    outs_per_step = {"round_flux": nface_local}.get(names[dom], cells_per_rank)
-    traffic = (per_out * outs_per_step * args.steps / max(1, launches[dom]) if per_out else None)
-    roofline = {"bound": "fp64", "kernel": f"round_gram_kernel ({names[dom]})",
+    outs_per_step = {"round_flux": nface_local}.get(dom, cells_per_rank)
+    traffic = (per_out * outs_per_step * args.steps / max(1, d_la) if per_out else None)
+    achieved = d_fl / d_ms / 1e9
+    roofline = {"bound": "fp64", "kernel": per_kernel[dom]["kernel"],
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak if fp64_peak else None,
-                "peak_source": "measured on this GPU by the DFMA probe in libttdvm_cuda.so",
-                "flops_per_launch": flops[dom] / max(1, launches[dom]),
-                "launch_ms": phase_ms[dom] / max(1, launches[dom]),
-                "algorithmic_bytes_per_launch": bytes_[dom] / max(1, launches[dom]),
-                "hbm_frac": (bytes_[dom] / dom_s / 1e9) / load_peaks().get("hbm_gbs", 6547.8)
-                if dom_s > 0 else None,
-                "traffic": traffic,
-                "phase_ms": {names[i]: round(float(phase_ms[i]), 3) for i in range(8)},
-                "phase_tflops": {names[i]: round(float(flops[i] / (phase_ms[i] / 1e3) / 1e12), 4)
-                                 for i in range(2, 7) if phase_ms[i] > 0}}
+                "peak_source": "measured on this GPU by the DFMA probe in libttdvm_cuda.so "
+                               "(MEASURED_PEAKS.json has no FP64 entry); hbm_frac against "
+                               "MEASURED_PEAKS.json hbm_gbs",
+                "flops_per_launch": d_fl / max(1, d_la), "launch_ms": d_ms / max(1, d_la),
+                "algorithmic_bytes_per_launch": d_by / max(1, d_la),
+                "hbm_frac": per_kernel[dom]["hbm_frac"], "traffic": traffic,
+                "measured_in": "a separate profiled pass over the same steps 1..K "
+                               "(per-phase CUDA events); the timed region runs unprofiled",
+                "profiled_ms_per_step": round(sum(v[0] for v in rep.values()) / args.steps, 3),
+                "per_kernel": per_kernel}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ncells = 2
-        rate, times = cpu_oracle_rate(args.config, args.scale, ncells, 1)
-        cpu = {"value": rate, "unit": "cell-steps/s", "cores": 1, "kind": "port",
-               "sample": f"{ncells} cells of the workload, one step from the initial state, "
-                         "numpy oracle (oracle/step.py), 1 process, 1 BLAS thread"}
+        # bounded: 2 blocks of 6^3 cells (~1.5k oblique normals of one-time
+        # set-up), the same warm-up and step counts as the GPU arm
+        threads = os.cpu_count() or 1
+        rate, info = cpu_reference_rate(p, 2, 6, args.warmup, args.steps, threads)
+        cpu = {"value": rate, "unit": "cell-steps/s", "cores": info["cores"],
+               "kind": info["kind"], "sample": info["sample"], "setup_s": info["setup_s"],
+               "max_rank_after": info["max_rank_after"]}
     if rank == 0:
         line = {"metric": "cell-steps/s", "value": value, "unit": "cell-steps/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -585,7 +772,7 @@ def main():
                                             else "single GPU"),
                                cells_total=ncell_total, cells_per_gpu=cells_per_rank,
                                max_rank_after=max_rank, setup_s=setup),
-                "roofline": roofline, "cpu_baseline": cpu,
+                "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
                 "e2e": {"value": e2e_value, "unit": "cell-steps/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "steps": args.e2e_steps},
                 "gpu_launches": gpu_launches, "clocks": clk.summary()}

@@ -188,6 +188,13 @@ int ttdvm_cuda_phase_times(ttdvm_ctx* ctx, double* ms8);
  * of the reference rounding algorithm on the actual ranks, compulsory HBM
  * bytes (inputs read once + outputs written once), and rounding launches. */
 int ttdvm_cuda_phase_work(ttdvm_ctx* ctx, double* flops8, double* bytes8, int32_t* launches8);
+/* Both of the above for the first nphase <= 9 phases; phase [8] is the
+ * wall-density kernel (wall_ghost, proj/src/boundary.cpp:84-101).  Phases
+ * 0, 1 and 8 report the algorithmic work of the moments (16 convolutions,
+ * cores read twice), the rank-4 f_S build (24 n doubles written per cell)
+ * and the wall inner products.  Any pointer may be NULL. */
+int ttdvm_cuda_phase_report(ttdvm_ctx* ctx, int32_t nphase, double* ms, double* flops,
+                            double* bytes, int32_t* launches);
 /* ttdvm_cuda_step timed with CUDA events on the library's stream (ms). */
 int ttdvm_cuda_timed_step(ttdvm_ctx* ctx, double dt, double eps, int32_t cap, int32_t nsteps,
                           double* ms);

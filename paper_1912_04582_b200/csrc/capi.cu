@@ -283,6 +283,8 @@ struct TermList {
 
 }  // namespace
 
+constexpr int kNPhase = 9;
+
 struct ttdvm_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
@@ -340,9 +342,11 @@ struct ttdvm_ctx {
   DevBuf<long long> d_tmp_off;
   DevBuf<double> d_tmp;
   bool profiling = false;
-  double phase_ms[8] = {0};
-  double phase_flops[8] = {0}, phase_bytes[8] = {0};
-  int phase_launches[8] = {0};
+  // phases: 0 moments, 1 f_S build, 2-6 roundings (f_S, collision, flux,
+  // residual, update), 7 bookkeeping, 8 wall densities
+  double phase_ms[kNPhase] = {0};
+  double phase_flops[kNPhase] = {0}, phase_bytes[kNPhase] = {0};
+  int phase_launches[kNPhase] = {0};
   DevBuf<double> d_acc;
   DevBuf<unsigned long long> d_prof;  // per-phase cycles of the rounding kernel
   bool round_prof = false;
@@ -399,7 +403,7 @@ struct Timer {
 };
 
 void reset_counters(ttdvm_ctx* c) {
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < kNPhase; ++i) {
     c->phase_ms[i] = 0.0;
     c->phase_flops[i] = 0.0;
     c->phase_bytes[i] = 0.0;
@@ -860,9 +864,20 @@ void run_collision(ttdvm_ctx* c, TensorSet& s, double eps, int count_ = -1) {
   {
     Timer t(c, 0);
     run_macro(c, s, c->d_macro.p, c->d_nu.p, count);
+    // algorithmic work: 16 convolutions of
+    // 2 (n r1 + n r1 r2 + r2 n) flops; the cores are read in two passes
+    const double doubles = (double)s.used * (s.count ? (double)count / s.count : 0.0);
+    c->phase_flops[0] += 32.0 * doubles;
+    c->phase_bytes[0] += 16.0 * doubles + 96.0 * count;
+    c->phase_launches[0] += 1;
   }
   {
     Timer t(c, 1);
+    // exact rank-4 f_S: 24 n doubles written per cell from 11 moments;
+    // ~6 flops per entry plus 3 n exponentials (~20 flops each)
+    c->phase_flops[1] += (double)count * n * (24.0 * 6.0 + 60.0);
+    c->phase_bytes[1] += (double)count * (24.0 * n + 11.0) * 8.0;
+    c->phase_launches[1] += 1;
     c->fsraw.resize(count);
     c->fsraw.arena.alloc(std::max<size_t>(1, (size_t)count * 24 * n));
     std::vector<int> rk(2 * (size_t)count, 4);
@@ -1433,9 +1448,15 @@ void step_fluxes_updates(ttdvm_ctx* c, TensorSet& s, TensorSet& nxt, double dt, 
                          int cap) {
   TensorSet* sets[kMaxSets] = {&s,         &c->fsraw,      &c->fs, &c->jr,  &c->phi,
                                 &c->res,    &c->freestream, &c->in, &c->xin, &c->eabs};
-  {
-    Timer t(c, 4);
+  if (c->nwall) {
+    Timer t(c, 8);
     run_walls(c, s, 0);
+    // n_w = <xi_n^+ o f> / -<xi_n^- o M>: two TT inner products per wall
+    // face against the cell's cores (ranks ~ maxr) and the face's factors
+    const double fsz = (double)c->n * (s.maxr1 + (double)s.maxr1 * s.maxr2 + s.maxr2);
+    c->phase_flops[8] += (double)c->nwall * 2.0 * 6.0 * fsz;
+    c->phase_bytes[8] += (double)c->nwall * 8.0 * (fsz + (double)c->wstride);
+    c->phase_launches[8] += 1;
   }
   if (c->nblocks <= 1) {
     {
@@ -2053,6 +2074,19 @@ int ttdvm_cuda_phase_work(ttdvm_ctx* c, double* flops8, double* bytes8, int32_t*
       if (flops8) flops8[i] = c->phase_flops[i];
       if (bytes8) bytes8[i] = c->phase_bytes[i];
       if (launches8) launches8[i] = c->phase_launches[i];
+    }
+  });
+}
+
+int ttdvm_cuda_phase_report(ttdvm_ctx* c, int32_t nphase, double* ms, double* flops,
+                            double* bytes, int32_t* launches) {
+  return guard(c, [&] {
+    require(nphase >= 0 && nphase <= kNPhase, "phase_report: at most 9 phases");
+    for (int i = 0; i < nphase; ++i) {
+      if (ms) ms[i] = c->phase_ms[i];
+      if (flops) flops[i] = c->phase_flops[i];
+      if (bytes) bytes[i] = c->phase_bytes[i];
+      if (launches) launches[i] = c->phase_launches[i];
     }
   });
 }

@@ -35,7 +35,7 @@ EXPORTS = (
     "ttdvm_cuda_timed_step", "ttdvm_cuda_fp64_peak", "ttdvm_cuda_round_profile",
     "ttdvm_cuda_set_owned", "ttdvm_cuda_set_blocks", "ttdvm_cuda_halo_pack", "ttdvm_cuda_halo_unpack",
     "ttdvm_cuda_face_factors", "ttdvm_cuda_wall_densities", "ttdvm_cuda_setup_info",
-    "ttdvm_cuda_round_resident",
+    "ttdvm_cuda_round_resident", "ttdvm_cuda_phase_report",
 )
 
 OK, EINVAL, EDOMAIN, ENOMEM, ECUDA, ENCCL = range(6)
@@ -101,6 +101,7 @@ def load_library(path: str = LIB_PATH):
         "ttdvm_cuda_wall_densities": (C.c_int, [vp, vp]),
         "ttdvm_cuda_setup_info": (C.c_int, [vp, vp]),
         "ttdvm_cuda_round_resident": (C.c_int, [vp, dbl, i32, i32, vp]),
+        "ttdvm_cuda_phase_report": (C.c_int, [vp, i32, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -368,6 +369,19 @@ class Context:
         la = np.zeros(8, dtype=np.int32)
         self._check(self.lib.ttdvm_cuda_phase_work(self.h, _ptr(fl), _ptr(by), _ptr(la)))
         return fl, by, la
+
+    PHASES = ("moments", "shakhov_build", "round_fs", "round_collision", "round_flux",
+              "round_residual", "round_update", "bookkeeping", "wall_densities")
+
+    def phase_report(self) -> dict:
+        """name -> (ms, flops, bytes, launches) of the last profiled call."""
+        k = len(self.PHASES)
+        ms, fl, by = np.zeros(k), np.zeros(k), np.zeros(k)
+        la = np.zeros(k, dtype=np.int32)
+        self._check(self.lib.ttdvm_cuda_phase_report(self.h, k, _ptr(ms), _ptr(fl), _ptr(by),
+                                                     _ptr(la)))
+        return {n: (float(ms[i]), float(fl[i]), float(by[i]), int(la[i]))
+                for i, n in enumerate(self.PHASES)}
 
     def fp64_peak(self) -> float:
         """Measured DFMA peak in TFLOP/s."""

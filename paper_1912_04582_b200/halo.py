@@ -70,3 +70,58 @@ def gpu_pack_unpack(ctx, device):
         ctx.halo_unpack(ids, ranks, offs, cores.data_ptr())
 
     return pack, unpack
+
+
+class HaloExchange:
+    """The per-step exchange of one rank over a CUDA-library context, with
+    every buffer preallocated and reused (core buffers grow geometrically as
+    the ranks rise): pack on the library's stream, one batched NCCL
+    send/recv of the (r1, r2) pairs, one of the cores, unpack.  The received
+    ranks cross to the host once (the library's unpack sizes the next
+    state's arena from them)."""
+
+    def __init__(self, ctx, part, device):
+        self.ctx, self.part, self.device = ctx, part, device
+        self.n = None
+        i32, f64 = torch.int32, torch.float64
+        self.send_r = {q: torch.empty(2 * len(ids), dtype=i32, device=device)
+                       for q, ids in part.send.items()}
+        self.recv_r = {q: torch.empty(2 * len(ids), dtype=i32, device=device)
+                       for q, ids in part.recv.items()}
+        self.recv_r_host = {q: torch.empty(2 * len(ids), dtype=i32, pin_memory=device.type == "cuda")
+                            for q, ids in part.recv.items()}
+        self.send_c = {q: torch.empty(1, dtype=f64, device=device) for q in part.send}
+        self.recv_c = {q: torch.empty(1, dtype=f64, device=device) for q in part.recv}
+
+    @staticmethod
+    def _fit(bufs, q, need, device):
+        if bufs[q].numel() < need:
+            bufs[q] = torch.empty(int(1.5 * need) + 1, dtype=torch.float64, device=device)
+        return bufs[q]
+
+    def exchange(self):
+        ctx, part, dev = self.ctx, self.part, self.device
+        n = ctx.n
+        sends = {}
+        for q, ids in part.send.items():
+            need = ctx.halo_size(ids)
+            buf = self._fit(self.send_c, q, need, dev)
+            ranks, _ = ctx.halo_pack(ids, buf.data_ptr(), need)  # synchronous on the library stream
+            self.send_r[q].copy_(torch.from_numpy(np.ascontiguousarray(ranks, dtype=np.int32)))
+            sends[q] = buf[:need]
+        _exchange(self.send_r, self.recv_r, dev)
+        sizes = {}
+        for q in part.recv:
+            self.recv_r_host[q].copy_(self.recv_r[q], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        for q in part.recv:
+            rk = self.recv_r_host[q].numpy().reshape(-1, 2).astype(np.int64)
+            off = np.zeros(rk.shape[0] + 1, dtype=np.int64)
+            off[1:] = np.cumsum(n * rk[:, 0] + n * rk[:, 0] * rk[:, 1] + rk[:, 1] * n)
+            sizes[q] = (rk.astype(np.int32).ravel(), off)
+        recvs = {q: self._fit(self.recv_c, q, int(sizes[q][1][-1]), dev)[:int(sizes[q][1][-1])]
+                 for q in part.recv}
+        _exchange(sends, recvs, dev)
+        torch.cuda.current_stream().synchronize()
+        for q, ids in part.recv.items():
+            ctx.halo_unpack(ids, sizes[q][0], sizes[q][1], recvs[q].data_ptr())
