@@ -11,6 +11,9 @@ stand in for them.
 Outputs:
   oracle/_ref/unit_tests     the reference's 50 doctest TEST_CASEs
                              (proj/tests/*.cpp) -- the gate of the oracle
+  oracle/_ref/dropin_step    oracle/dropin_step.cpp: the product's drop-in adapter
+                             (include/ttdvm_cuda_adapter.hpp) on the reference's
+                             own types against the reference S1 step
   oracle/_ref/libttdvm_ref.so  proj/src/{tt_tensor,physics,velocity_grid,
                              boundary,mesh}.cpp + oracle/ref_step.cpp (the S1
                              step composed of reference API calls, C ABI for
@@ -41,6 +44,7 @@ FLAGS = ["-std=gnu++20", "-O3", "-march=x86-64-v3", "-ffp-contract=off", "-fPIC"
          "-I", os.path.join(HERE, "shim"), "-I", os.path.join(PROJ, "include")]
 LIB = os.path.join(OUT, "libttdvm_ref.so")
 UNIT = os.path.join(OUT, "unit_tests")
+DROPIN = os.path.join(OUT, "dropin_step")
 
 
 def _newer(target: str, deps) -> bool:
@@ -92,7 +96,28 @@ def build(force: bool = False) -> tuple[str, str]:
         subprocess.run([CXX, "-shared", "-fopenmp", *src_objs, step_o, "-o", LIB], check=True)
     if force or not _newer(UNIT, src_objs + test_objs):
         subprocess.run([CXX, "-fopenmp", *test_objs, *src_objs, "-o", UNIT], check=True)
+    build_dropin(src_objs, force)
     return LIB, UNIT
+
+
+def build_dropin(src_objs, force: bool = False):
+    """oracle/_ref/dropin_step: include/ttdvm_cuda_adapter.hpp (the drop-in
+    on the reference's own types) compiled against proj/include and linked
+    with the reference objects and the product's libttdvm_cuda.so."""
+    root = os.path.dirname(HERE)
+    prod = os.path.join(root, "paper_1912_04582_b200")
+    cuda_lib = os.path.join(prod, "libttdvm_cuda.so")
+    src = os.path.join(HERE, "dropin_step.cpp")
+    inc = os.path.join(root, "include")
+    if not os.path.exists(cuda_lib):
+        return None
+    deps = [src, cuda_lib, *src_objs, *_shim_headers(),
+            *(os.path.join(inc, f) for f in os.listdir(inc))]
+    if not force and _newer(DROPIN, deps):
+        return DROPIN
+    subprocess.run([CXX, *FLAGS, "-I", inc, src, *src_objs, "-L", prod, "-lttdvm_cuda",
+                    "-Wl,-rpath,$ORIGIN/../../paper_1912_04582_b200", "-o", DROPIN], check=True)
+    return DROPIN
 
 
 def run_unit_tests() -> subprocess.CompletedProcess:
