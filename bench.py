@@ -582,6 +582,7 @@ def main():
     setup = {"mesh_and_state_s": round(time.perf_counter() - t_setup, 2)}
     ctx = Context(local)
     part = None
+    hx = None  # torch.distributed halo exchange (A/B only; the default is inside the library)
     scaling = "weak"
     ncell_total = p.mesh.ncell
     if world > 1:
@@ -607,10 +608,20 @@ def main():
         ctx.set_gas(pg.gas)
         ctx.set_mesh(part.mesh)
         ctx.set_bcs(pg.bcs)
-        ctx.set_owned(part.n_owned)
         f_local = local_state(part, pg.f0)
+        # halo exchange inside the library: NCCL communicator from a unique id
+        # made by rank 0, the halo plan of this rank's part; every step then
+        # starts with the exchange, overlapped with the collision phases
+        # (TTDVM_HALO=python keeps the torch.distributed exchange for A/B)
+        if os.environ.get("TTDVM_HALO", "library") == "python":
+            ctx.set_owned(part.n_owned)
+            hx = halo.HaloExchange(ctx, part, torch.device("cuda", local))
+        else:
+            uid = [Context.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ctx.comm_init(world, rank, uid[0])
+            ctx.set_partition(part.n_owned, part.send, part.recv)
         ctx.upload_state(f_local)
-        hx = halo.HaloExchange(ctx, part, torch.device("cuda", local))
         p = pg
         cells_per_rank = part.n_owned
     else:
@@ -626,7 +637,7 @@ def main():
 
     def run_steps(k):
         """k steps; device ms by CUDA events on the stream the kernels run on."""
-        if part is None:
+        if part is None or hx is None:
             return ctx.timed_step(p.dt, p.eps, p.cap, k)
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
@@ -649,7 +660,7 @@ def main():
     with ClockSampler(local) as clk:
         ms = run_steps(args.steps)
     torch.cuda.synchronize()
-    gpu_launches = ctx.launch_count() * (1 if part is None else args.steps)
+    gpu_launches = ctx.launch_count() * (1 if (part is None or hx is None) else args.steps)
     setup["cell_blocks"] = ctx.setup_info()["cell_blocks"]  # grown on out-of-memory
     if dist:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -674,7 +685,7 @@ def main():
         h2d += int(host.cores.nbytes + host.ranks.nbytes + host.offsets.nbytes)
         ctx.upload_state(host)
         ctx.step(p.dt, p.eps, p.cap, 1)
-        if part is not None:
+        if hx is not None:
             hx.exchange()
         host = ctx.download_state(out=pinned)
         d2h += int(host.cores.nbytes + host.ranks.nbytes + host.offsets.nbytes)
@@ -700,11 +711,11 @@ def main():
     for chunk in (args.steps - 1, 1):
         if chunk <= 0:
             continue
-        if part is None:
+        if part is None or hx is None:
             ctx.timed_step(p.dt, p.eps, p.cap, chunk)
             r = ctx.phase_report()
             rep = r if rep is None else {k: tuple(a + b for a, b in zip(rep[k], r[k])) for k in r}
-            if chunk == args.steps - 1:
+            if chunk == args.steps - 1 and part is None:
                 st_prev = ctx.download_state()
         else:
             for _ in range(chunk):
@@ -770,6 +781,7 @@ def main():
                                              f"x-slab partition x{world}") +
                                             ", halo TT cores over NCCL" if world > 1
                                             else "single GPU"),
+                               halo=(ctx.halo_stats() if part is not None and hx is None else None),
                                cells_total=ncell_total, cells_per_gpu=cells_per_rank,
                                max_rank_after=max_rank, setup_s=setup),
                 "roofline": roofline, "cpu_baseline": cpu, "parity": parity,

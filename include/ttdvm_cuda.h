@@ -54,8 +54,7 @@ typedef struct {
   double free_n, free_t, free_u[3];
 } ttdvm_bc;
 
-/* Context lifetime.  device = CUDA ordinal; nccl_comm = NULL or an
- * ncclComm_t for the multi-GPU halo exchange (ttdvm_cuda_set_partition). */
+/* Context lifetime.  device = CUDA ordinal.  One context per GPU / rank. */
 int ttdvm_cuda_create(int device, ttdvm_ctx** out);
 int ttdvm_cuda_destroy(ttdvm_ctx* ctx);
 const char* ttdvm_cuda_last_error(const ttdvm_ctx* ctx);
@@ -104,11 +103,45 @@ int ttdvm_cuda_step(ttdvm_ctx* ctx, double dt, double eps, int32_t cap, int32_t 
  * intermediate in host memory). */
 int ttdvm_cuda_set_blocks(ttdvm_ctx* ctx, int32_t nblocks);
 
-/* Multi-GPU slab partition: cells [0, nowned) of the
- * mesh are stepped, the rest are halo ghosts whose states the caller
- * refreshes after every step with the two calls below (packed in the
- * ttdvm_tt_batch layout into / out of caller-provided DEVICE buffers that
- * the caller exchanges with NCCL).  Ghosts carry over unchanged otherwise. */
+/* ---- Multi-GPU spatial partition (no reference
+ * counterpart: the reference is single-process, PAPER.md:478 lists multi-GPU
+ * as future work).  One process and one context per GPU; cells [0, nowned)
+ * of the context's (local) mesh are stepped, the rest are ghosts behind cut
+ * faces.
+ *
+ * In-library exchange over NCCL: rank 0 makes a unique id
+ * (ttdvm_cuda_nccl_unique_id), shares its 128 bytes out of band, every rank
+ * joins with ttdvm_cuda_comm_init (or hands over an existing ncclComm_t with
+ * ttdvm_cuda_set_comm) and installs its halo plan with
+ * ttdvm_cuda_set_partition.  Every ttdvm_cuda_step then begins by exchanging
+ * the ghost cells of the state it starts from -- the (r1, r2) pairs, then the
+ * packed cores, grouped ncclSend/ncclRecv on a communication stream --
+ * overlapped with the moments, f_S and collision roundings of the owned
+ * cells; the face fluxes wait for the halo.  A failure on any rank
+ * (nonpositive density, out of memory, ...) reaches every rank through an
+ * ncclAllReduce(max) of the status code at the end of the step.  libnccl is
+ * bound at run time (dlopen of libnccl.so.2; TTDVM_NCCL_LIB overrides):
+ * TTDVM_ENCCL when it is missing or a call fails. */
+int ttdvm_cuda_nccl_unique_id(char* id128);
+int ttdvm_cuda_comm_init(ttdvm_ctx* ctx, int32_t nranks, int32_t rank, const char* id128);
+/* nccl_comm: an ncclComm_t the caller owns (NULL detaches). */
+int ttdvm_cuda_set_comm(ttdvm_ctx* ctx, void* nccl_comm, int32_t nranks, int32_t rank);
+/* Halo plan: per peer q (rank peer_rank[q]) the owned local cells to send,
+ * send_ids[send_off[q] .. send_off[q+1]), and the ghost local cells to fill,
+ * recv_ids[recv_off[q] .. recv_off[q+1]); both sides list a pair's cells in
+ * the same order (ascending global id).  Also sets nowned. */
+int ttdvm_cuda_set_partition(ttdvm_ctx* ctx, int32_t nowned, int32_t npeers,
+                             const int32_t* peer_rank, const int64_t* send_off,
+                             const int32_t* send_ids, const int64_t* recv_off,
+                             const int32_t* recv_ids);
+/* [0] exchanges, [1] bytes sent, [2] bytes received, [3] host ms spent in
+ * the exchange (issue + waits), since the context was created. */
+int ttdvm_cuda_halo_stats(ttdvm_ctx* ctx, double* out4);
+
+/* Caller-driven alternative (no communicator set): the caller refreshes
+ * the ghosts after every step with the calls below (packed in the
+ * ttdvm_tt_batch layout into / out of caller-provided DEVICE buffers that it
+ * exchanges itself).  Ghosts carry over unchanged otherwise. */
 int ttdvm_cuda_set_owned(ttdvm_ctx* ctx, int32_t nowned);
 /* Pack the current states of cells ids[0..count) into dev_dst; fills
  * ranks_out[2*count] and offsets_out[count+1] (doubles).  ENOMEM with

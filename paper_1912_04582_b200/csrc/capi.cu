@@ -9,6 +9,7 @@
 // launch sets a flag, the host grows that arena and repeats the launch.
 // The state is double-buffered across steps.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -285,6 +286,22 @@ struct TermList {
 
 constexpr int kNPhase = 9;
 
+// One peer of the halo plan: the owned local cells it needs from this rank
+// and the ghost local cells it fills here, both in the order the two sides
+// agreed on (ascending global id, partition.build_part).
+struct HaloPeer {
+  int rank = -1;
+  std::vector<int> send_ids, recv_ids;
+  DevBuf<int> d_send_ids;
+  DevBuf<int> d_send_rk, d_recv_rk;   // (r1, r2) pairs
+  std::vector<int> h_send_rk;
+  int* h_recv_rk = nullptr;           // pinned
+  DevBuf<long long> d_send_off;
+  std::vector<long long> h_send_off, h_recv_off;
+  DevBuf<double> send_buf, recv_buf;
+  long long send_doubles = 0, recv_doubles = 0;
+};
+
 struct ttdvm_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
@@ -353,6 +370,22 @@ struct ttdvm_ctx {
   int cur_phase = 7;
   long long launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // multi-GPU halo exchange inside the library: the
+  // NCCL communicator (created here from a unique id, or adopted), the halo
+  // plan per peer and preallocated device / pinned buffers
+  void* comm = nullptr;  // ncclComm_t
+  bool own_comm = false;
+  int nranks = 1, rank = 0;
+  std::vector<HaloPeer> peers;
+  cudaStream_t comm_st = nullptr;
+  cudaEvent_t halo_ready = nullptr, halo_done = nullptr;
+  bool halo_pending = false;
+  int* h_rk_all = nullptr;  // pinned, 2 * ncell
+  size_t h_rk_all_n = 0;
+  DevBuf<int> d_flag;
+  int* h_flag = nullptr;  // pinned
+  double halo_ms = 0.0;
+  long long halo_bytes_sent = 0, halo_bytes_recv = 0, halo_exchanges = 0;
   // auxiliary streams for concurrent rank bins (run_round), created lazily
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t fork_ev = nullptr, join_ev[3] = {nullptr, nullptr, nullptr};
@@ -554,6 +587,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   struct Launch {
     int bin, count, rm1, rm2, ms, jb;
     bool spill, wide, narrow;
+    int oc = 0;  // doubles of the operand cache (TMA bulk copies of whole operands), 0 = off
   };
   // 256-thread CTAs from Gram dimension TTDVM_WIDE_D (default 16) up: the
   // measured crossover between the short-phase small tiles (128 threads, four
@@ -586,16 +620,33 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   // plan would leave fewer CTAs per SM than the variant's launch bounds --
   // or than the JB = 1 plan itself fits (then the spare shared memory goes
   // to larger slice batches: config 3, +6 %)
-  auto pick_jb = [&](const Launch& l) {
-    const size_t base = round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false);
+  // (oc: bytes of the operand cache the plan must also hold; *ctas returns
+  // the CTAs per SM the chosen plan fits)
+  auto pick_jb = [&](const Launch& l, size_t oc = 0, int* ctas = nullptr) {
+    const size_t base = round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false) + oc;
     const int fit1 = std::max(1, (int)(228 * 1024 / (base + 1024)));
     const int k = std::min(blocks_per_sm(l.rm1, l.rm2), fit1);
     const size_t budget =
         std::max(base, std::min(kSmemMax, (size_t)(228 * 1024 / k) - 2048));
     int jb = (n + 3) / 4;
-    while (jb > 1 && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, jb, false) > budget) --jb;
+    while (jb > 1 && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, jb, false) + oc > budget) --jb;
+    if (ctas) *ctas = k;
     return jb;
   };
+  // Operand cache (round.cu): every distinct operand tensor of an output is
+  // fetched whole into shared memory by one cp.async.bulk (TMA).  Taken when
+  // the bin's largest operand set fits without costing a CTA per SM or a
+  // slice of the batch.  Measured (config 4, half scale, same box,
+  // scripts/gpu_r2_oc.sh): where the cache halves the slice batch -- the D = 12
+  // face-flux bin, JB 10 -> 5 -- the phase slows by 20 % (the L1 prefetch at
+  // set-up already hides the operands' latency; the barrier phases saved by
+  // larger slice batches matter more); where the batch is kept (the D = 16
+  // residual bin) it is neutral to -3 %.  TTDVM_OPCACHE=0 turns it off, =2
+  // forces it wherever it fits at all (A/B).
+  static const int opcache_mode = [] {
+    const char* e = getenv("TTDVM_OPCACHE");
+    return e ? atoi(e) : 1;
+  }();
   std::vector<Launch> plan;
   for (int b = kRankBins - 1; b >= 0; --b) {  // large ranks first (long CTAs start early)
     if (!bcount[b]) continue;
@@ -610,15 +661,27 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     l.spill = !use_tsqr &&
               round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false) > kSmemMax;
     if (l.spill) l.narrow = false;
-    if (!use_tsqr && !l.spill) l.jb = pick_jb(l);
+    if (!use_tsqr && !l.spill) {
+      int k0 = 1, k1 = 1;
+      l.jb = pick_jb(l, 0, &k0);
+      const size_t ocb = 8 * (size_t)((std::max(0, bm[4]) + 1) & ~1);
+      if (opcache_mode > 0 && bm[4] > 0 &&
+          round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false) + ocb <= kSmemMax) {
+        const int jb1 = pick_jb(l, ocb, &k1);
+        if (opcache_mode >= 2 || (k1 >= k0 && jb1 >= l.jb)) {
+          l.oc = bm[4];
+          l.jb = jb1;
+        }
+      }
+    }
     static const int force_jb = [] {  // diagnostics: TTDVM_JB=k forces k slices per phase
       const char* e = getenv("TTDVM_JB");
       return e ? atoi(e) : 0;
     }();
     if (force_jb > 0 && !use_tsqr && !l.spill) {
       l.jb = std::min(n, force_jb);
-      while (l.jb > 1 &&
-             round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, l.jb, false) > kSmemMax)
+      while (l.jb > 1 && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, l.jb, false) +
+                                 8 * (size_t)((l.oc + 1) & ~1) > kSmemMax)
         --l.jb;
     }
     if (l.spill && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, true) > kSmemMax)
@@ -740,6 +803,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
         a.RM2 = l.rm2;
         a.MSMAX = l.ms;
         a.JB = l.jb;
+        a.OC = l.spill ? 0 : l.oc;
         a.olist = c->d_olist.p + (size_t)l.bin * nout;
         a.gscratch = nullptr;
         a.gstride = 0;
@@ -774,9 +838,9 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
           cudaEventDestroy(d0);
           cudaEventDestroy(d1);
           fprintf(stderr,
-                  "[ttdvm bin] phase %d bin %d outputs %d summed ranks %dx%d D %d jb %d %s%s grid %d:"
+                  "[ttdvm bin] phase %d bin %d outputs %d summed ranks %dx%d D %d jb %d oc %d %s%s grid %d:"
                   " %.2f ms\n",
-                  c->cur_phase, l.bin, l.count, l.rm1, l.rm2, gram_d(l.rm1, l.rm2), l.jb,
+                  c->cur_phase, l.bin, l.count, l.rm1, l.rm2, gram_d(l.rm1, l.rm2), l.jb, l.oc,
                   l.wide ? "g256" : (l.narrow ? "g32" : "g128"), l.spill ? " spill" : "", grid, ms);
         }
       }
@@ -1500,6 +1564,236 @@ void step_fluxes_updates(ttdvm_ctx* c, TensorSet& s, TensorSet& nxt, double dt, 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Multi-GPU: halo exchange of TT cores over NCCL inside the library
+// (the reference is single-process, PAPER.md:478 lists
+// multi-GPU as future work).  libnccl is bound at run time (dlopen), so a
+// single-GPU build or host has no NCCL dependency.
+struct ncclUniqueIdBytes {  // ncclUniqueId (nccl.h): 128 opaque bytes, passed by value
+  char internal[128];
+};
+struct NcclApi {
+  void* lib = nullptr;
+  int (*GetUniqueId)(void*) = nullptr;
+  int (*CommInitRank)(void**, int, ncclUniqueIdBytes, int) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+// nccl.h constants (stable across NCCL 2.x): ncclInt32 = 2, ncclFloat64 = 8, ncclMax = 2
+constexpr int kNcclInt32 = 2, kNcclFloat64 = 8, kNcclMax = 2;
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    const char* names[] = {getenv("TTDVM_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      if (!nm || !*nm) continue;
+      a.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (a.lib) break;
+    }
+    if (!a.lib) return a;
+    auto sym = [&](const char* n) { return dlsym(a.lib, n); };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    return a;
+  }();
+  return api;
+}
+
+void require_nccl() {
+  NcclApi& a = nccl();
+  if (!a.lib || !a.GetUniqueId || !a.CommInitRank || !a.Send || !a.Recv || !a.AllReduce ||
+      !a.GroupStart || !a.GroupEnd)
+    throw Fail{TTDVM_ENCCL, "libnccl.so.2 could not be loaded (set TTDVM_NCCL_LIB or LD_LIBRARY_PATH)"};
+}
+
+#define NK(x)                                                                          \
+  do {                                                                                 \
+    const int r_ = (x);                                                                \
+    if (r_ != 0)                                                                       \
+      throw Fail{TTDVM_ENCCL, std::string(#x) + ": " +                                 \
+                                  (nccl().GetErrorString ? nccl().GetErrorString(r_) : "NCCL error")}; \
+  } while (0)
+
+void ensure_comm_stream(ttdvm_ctx* c) {
+  if (c->comm_st) return;
+  CK(cudaStreamCreateWithFlags(&c->comm_st, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->halo_ready, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->halo_done, cudaEventDisableTiming));
+  c->d_flag.alloc(2);
+  CK(cudaMallocHost(&c->h_flag, 2 * sizeof(int)));
+}
+
+void free_peers(ttdvm_ctx* c) {
+  for (HaloPeer& p : c->peers) {
+    p.d_send_ids.free();
+    p.d_send_rk.free();
+    p.d_recv_rk.free();
+    p.d_send_off.free();
+    p.send_buf.free();
+    p.recv_buf.free();
+    if (p.h_recv_rk) cudaFreeHost(p.h_recv_rk);
+  }
+  c->peers.clear();
+}
+
+// Start the exchange of the ghost cells of `s` (the state the step starts
+// from): (1) the (r1, r2) pairs of the cells every peer needs, one grouped
+// ncclSend/ncclRecv, read back so both sides know the packed sizes; (2) the
+// send cells' cores are gathered into per-peer buffers on the compute stream
+// and go out in one grouped ncclSend/ncclRecv on the communication stream.
+// Returns with phase (2) in flight: the moments, f_S and collision roundings
+// of the owned cells -- which read no ghost -- overlap it.  The state arena
+// is grown for the incoming ghosts here, before those kernels are queued.
+void halo_begin(ttdvm_ctx* c, TensorSet& s) {
+  if (!c->comm || c->peers.empty()) return;
+  NcclApi& a = nccl();
+  const int n = c->n;
+  ensure_comm_stream(c);
+  const auto t0 = std::chrono::steady_clock::now();
+  if (c->h_rk_all_n < 2 * (size_t)s.count) {
+    if (c->h_rk_all) cudaFreeHost(c->h_rk_all);
+    CK(cudaMallocHost(&c->h_rk_all, 2 * (size_t)s.count * sizeof(int)));
+    c->h_rk_all_n = 2 * (size_t)s.count;
+  }
+  CK(cudaMemcpyAsync(c->h_rk_all, s.ranks.p, 8LL * s.count, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  for (HaloPeer& p : c->peers) {
+    const int ns = (int)p.send_ids.size();
+    p.h_send_rk.resize(2 * (size_t)ns);
+    p.h_send_off.resize((size_t)ns + 1);
+    long long o = 0;
+    for (int i = 0; i < ns; ++i) {
+      const int r1 = c->h_rk_all[2 * p.send_ids[i]], r2 = c->h_rk_all[2 * p.send_ids[i] + 1];
+      p.h_send_rk[2 * i] = r1;
+      p.h_send_rk[2 * i + 1] = r2;
+      p.h_send_off[i] = o;
+      o += tt_size(n, n, n, r1, r2);
+    }
+    p.h_send_off[ns] = o;
+    p.send_doubles = o;
+    if (ns) {
+      CK(cudaMemcpyAsync(p.d_send_rk.p, p.h_send_rk.data(), 8LL * ns, cudaMemcpyHostToDevice, c->st));
+      CK(cudaMemcpyAsync(p.d_send_off.p, p.h_send_off.data(), 8LL * ns, cudaMemcpyHostToDevice, c->st));
+    }
+  }
+  // phase 1: ranks
+  CK(cudaEventRecord(c->halo_ready, c->st));
+  CK(cudaStreamWaitEvent(c->comm_st, c->halo_ready, 0));
+  NK(a.GroupStart());
+  for (HaloPeer& p : c->peers) {
+    if (!p.send_ids.empty())
+      NK(a.Send(p.d_send_rk.p, 2 * p.send_ids.size(), kNcclInt32, p.rank, c->comm, c->comm_st));
+    if (!p.recv_ids.empty())
+      NK(a.Recv(p.d_recv_rk.p, 2 * p.recv_ids.size(), kNcclInt32, p.rank, c->comm, c->comm_st));
+  }
+  NK(a.GroupEnd());
+  for (HaloPeer& p : c->peers)
+    if (!p.recv_ids.empty())
+      CK(cudaMemcpyAsync(p.h_recv_rk, p.d_recv_rk.p, 8LL * p.recv_ids.size(), cudaMemcpyDeviceToHost,
+                         c->comm_st));
+  CK(cudaStreamSynchronize(c->comm_st));
+  long long incoming = 0;
+  for (HaloPeer& p : c->peers) {
+    const int nr = (int)p.recv_ids.size();
+    p.h_recv_off.resize((size_t)nr + 1);
+    long long o = 0;
+    for (int i = 0; i < nr; ++i) {
+      const int r1 = p.h_recv_rk[2 * i], r2 = p.h_recv_rk[2 * i + 1];
+      if (r1 < 1 || r2 < 1 || r1 > 4 * n || r2 > 4 * n)
+        throw Fail{TTDVM_ENCCL, "halo exchange: implausible ranks received from rank " +
+                                    std::to_string(p.rank)};
+      p.h_recv_off[i] = o;
+      o += tt_size(n, n, n, r1, r2);
+    }
+    p.h_recv_off[nr] = o;
+    p.recv_doubles = o;
+    incoming += o;
+    p.send_buf.alloc(std::max<size_t>(1, (size_t)p.send_doubles));
+    p.recv_buf.alloc(std::max<size_t>(1, (size_t)p.recv_doubles));
+    c->halo_bytes_sent += 8 * p.send_doubles + 8LL * (long long)p.send_ids.size();
+    c->halo_bytes_recv += 8 * p.recv_doubles + 8LL * nr;
+  }
+  // room for the incoming ghosts now: no arena regrowth while the collision
+  // kernels read the owned cells
+  grow_preserve(c, s, s.used, s.used + incoming);
+  // phase 2: cores
+  for (HaloPeer& p : c->peers) {
+    if (p.send_ids.empty()) continue;
+    CK(launch_gather_ids(s.view(), p.d_send_ids.p, (int)p.send_ids.size(), p.d_send_off.p, n, n, n,
+                         p.send_buf.p, c->st));
+    c->launches += 1;
+  }
+  CK(cudaEventRecord(c->halo_ready, c->st));
+  CK(cudaStreamWaitEvent(c->comm_st, c->halo_ready, 0));
+  NK(a.GroupStart());
+  for (HaloPeer& p : c->peers) {
+    if (p.send_doubles)
+      NK(a.Send(p.send_buf.p, (size_t)p.send_doubles, kNcclFloat64, p.rank, c->comm, c->comm_st));
+    if (p.recv_doubles)
+      NK(a.Recv(p.recv_buf.p, (size_t)p.recv_doubles, kNcclFloat64, p.rank, c->comm, c->comm_st));
+  }
+  NK(a.GroupEnd());
+  CK(cudaEventRecord(c->halo_done, c->comm_st));
+  c->halo_pending = true;
+  c->halo_exchanges += 1;
+  c->halo_ms +=
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Wait for the cores and place them as the ghost entries of `s`.
+void halo_end(ttdvm_ctx* c, TensorSet& s) {
+  if (!c->halo_pending) return;
+  c->halo_pending = false;
+  const auto t0 = std::chrono::steady_clock::now();
+  CK(cudaStreamWaitEvent(c->st, c->halo_done, 0));
+  for (HaloPeer& p : c->peers) {
+    if (p.recv_ids.empty()) continue;
+    TSet src;
+    src.ranks = p.d_recv_rk.p;
+    src.off = nullptr;
+    src.base = p.recv_buf.p;
+    src.tscale = nullptr;
+    src.uscale = 1.0;
+    DevBuf<long long> of;  // source offsets on the device
+    of.alloc(p.recv_ids.size());
+    CK(cudaMemcpy(of.p, p.h_recv_off.data(), 8LL * p.recv_ids.size(), cudaMemcpyHostToDevice));
+    src.off = of.p;
+    append_tensors(c, src, nullptr, (int)p.recv_ids.size(), p.h_recv_rk, p.recv_ids.data(), s);
+    of.retire();
+  }
+  c->halo_ms +=
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// max over ranks of a status code: a rank that failed inside its step skips
+// to this point, its peers finish theirs, and every rank then reports the
+// failure together instead of waiting for a halo that never comes.
+int allreduce_status(ttdvm_ctx* c, int local) {
+  if (!c->comm) return local;
+  NcclApi& a = nccl();
+  ensure_comm_stream(c);
+  c->h_flag[0] = local;
+  CK(cudaMemcpyAsync(c->d_flag.p, c->h_flag, sizeof(int), cudaMemcpyHostToDevice, c->comm_st));
+  NK(a.AllReduce(c->d_flag.p, c->d_flag.p + 1, 1, kNcclInt32, kNcclMax, c->comm, c->comm_st));
+  CK(cudaMemcpyAsync(c->h_flag + 1, c->d_flag.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c->comm_st));
+  CK(cudaStreamSynchronize(c->comm_st));
+  return c->h_flag[1];
+}
+
 void step_once(ttdvm_ctx* c, double dt, double eps, int cap) {
   TensorSet& s = c->state[c->cur];
   TensorSet& nxt = c->state[1 - c->cur];
@@ -1507,8 +1801,10 @@ void step_once(ttdvm_ctx* c, double dt, double eps, int cap) {
   // pieces (3) + (4): moments, f_S, J_r = round(f_S - f) over the owned
   // cells; nu applied as J's per-tensor scale (TtTensor::scaled after
   // rounding, physics.cpp:118)
+  halo_begin(c, s);  // ghosts of t^n in flight while the owned cells' collision terms run
   run_collision(c, s, eps, nown);
   c->jr.tscale = c->d_nu.p;
+  halo_end(c, s);
   for (;;) {
     try {
       step_fluxes_updates(c, s, nxt, dt, eps, cap);
@@ -1541,6 +1837,30 @@ void step_once(ttdvm_ctx* c, double dt, double eps, int cap) {
     sid.free();
   }
   c->cur = 1 - c->cur;
+}
+
+// One step; with a communicator, every rank learns of a failure on any rank
+// (ncclAllReduce max of the status code) and fails with it.
+void step_synced(ttdvm_ctx* c, double dt, double eps, int cap) {
+  if (!c->comm) {
+    step_once(c, dt, eps, cap);
+    return;
+  }
+  Fail local{TTDVM_OK, ""};
+  try {
+    step_once(c, dt, eps, cap);
+  } catch (const Fail& e) {
+    local = e;
+    if (c->halo_pending) {  // drain the exchange this rank started
+      cudaStreamSynchronize(c->comm_st);
+      c->halo_pending = false;
+    }
+  }
+  const int global = allreduce_status(c, local.code);
+  if (local.code != TTDVM_OK) throw local;
+  if (global != TTDVM_OK)
+    throw Fail{global, "explicit_step failed on another rank of the partition (status " +
+                           std::to_string(global) + ")"};
 }
 
 void layout_of(ttdvm_ctx* c, const TensorSet& s, int32_t* ranks, int64_t* offsets) {
@@ -1653,6 +1973,17 @@ int ttdvm_cuda_destroy(ttdvm_ctx* c) {
   c->d_tmp.free();
   c->d_tmp_off.free();
   if (c->h_status) cudaFreeHost(c->h_status);
+  free_peers(c);
+  if (c->comm_st) {
+    cudaStreamSynchronize(c->comm_st);
+    cudaStreamDestroy(c->comm_st);
+    cudaEventDestroy(c->halo_ready);
+    cudaEventDestroy(c->halo_done);
+    cudaFreeHost(c->h_flag);
+  }
+  c->d_flag.free();
+  if (c->h_rk_all) cudaFreeHost(c->h_rk_all);
+  if (c->comm && c->own_comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
   if (c->fork_ev) {
@@ -1765,7 +2096,7 @@ int ttdvm_cuda_step(ttdvm_ctx* c, double dt, double eps, int32_t cap, int32_t ns
     cudaSetDevice(c->device);
     build_step_terms(c);
     reset_counters(c);
-    for (int k = 0; k < nsteps; ++k) step_once(c, dt, eps, cap);
+    for (int k = 0; k < nsteps; ++k) step_synced(c, dt, eps, cap);
   });
 }
 
@@ -2003,6 +2334,94 @@ int ttdvm_cuda_set_blocks(ttdvm_ctx* c, int32_t nblocks) {
   });
 }
 
+int ttdvm_cuda_nccl_unique_id(char* id128) {
+  try {
+    require_nccl();
+    if (!id128) return TTDVM_EINVAL;
+    ncclUniqueIdBytes id;
+    if (nccl().GetUniqueId(&id) != 0) return TTDVM_ENCCL;
+    memcpy(id128, id.internal, 128);
+    return TTDVM_OK;
+  } catch (const Fail& e) {
+    return e.code;
+  }
+}
+
+int ttdvm_cuda_comm_init(ttdvm_ctx* c, int32_t nranks, int32_t rank, const char* id128) {
+  return guard(c, [&] {
+    require(id128 && nranks >= 1 && rank >= 0 && rank < nranks, "comm_init: bad rank / id");
+    require_nccl();
+    cudaSetDevice(c->device);
+    if (c->comm && c->own_comm) nccl().CommDestroy(c->comm);
+    c->comm = nullptr;
+    ncclUniqueIdBytes id;
+    memcpy(id.internal, id128, 128);
+    void* comm = nullptr;
+    NK(nccl().CommInitRank(&comm, nranks, id, rank));
+    c->comm = comm;
+    c->own_comm = true;
+    c->nranks = nranks;
+    c->rank = rank;
+    ensure_comm_stream(c);
+  });
+}
+
+int ttdvm_cuda_set_comm(ttdvm_ctx* c, void* nccl_comm, int32_t nranks, int32_t rank) {
+  return guard(c, [&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "set_comm: bad rank");
+    if (nccl_comm) require_nccl();
+    cudaSetDevice(c->device);
+    if (c->comm && c->own_comm) nccl().CommDestroy(c->comm);
+    c->comm = nccl_comm;
+    c->own_comm = false;
+    c->nranks = nranks;
+    c->rank = rank;
+    if (nccl_comm) ensure_comm_stream(c);
+  });
+}
+
+int ttdvm_cuda_set_partition(ttdvm_ctx* c, int32_t nowned, int32_t npeers, const int32_t* peer_rank,
+                             const int64_t* send_off, const int32_t* send_ids,
+                             const int64_t* recv_off, const int32_t* recv_ids) {
+  return guard(c, [&] {
+    require(nowned >= 1 && nowned <= c->ncell, "owned cell count out of range");
+    require(npeers >= 0 && (npeers == 0 || (peer_rank && send_off && recv_off)),
+            "set_partition: null halo plan");
+    cudaSetDevice(c->device);
+    free_peers(c);
+    c->nowned = nowned;
+    c->terms_dirty = true;
+    c->peers.resize(npeers);
+    for (int q = 0; q < npeers; ++q) {
+      HaloPeer& p = c->peers[q];
+      p.rank = peer_rank[q];
+      require(p.rank >= 0 && p.rank < std::max(1, c->nranks), "set_partition: peer rank out of range");
+      p.send_ids.assign(send_ids + send_off[q], send_ids + send_off[q + 1]);
+      p.recv_ids.assign(recv_ids + recv_off[q], recv_ids + recv_off[q + 1]);
+      for (int id : p.send_ids) require(id >= 0 && id < nowned, "set_partition: send id is not an owned cell");
+      for (int id : p.recv_ids)
+        require(id >= nowned && id < c->ncell, "set_partition: recv id is not a ghost cell");
+      const size_t ns = p.send_ids.size(), nr = p.recv_ids.size();
+      p.d_send_ids.alloc(std::max<size_t>(1, ns));
+      p.d_send_rk.alloc(std::max<size_t>(1, 2 * ns));
+      p.d_recv_rk.alloc(std::max<size_t>(1, 2 * nr));
+      p.d_send_off.alloc(std::max<size_t>(1, ns));
+      if (ns) CK(cudaMemcpy(p.d_send_ids.p, p.send_ids.data(), 4 * ns, cudaMemcpyHostToDevice));
+      CK(cudaMallocHost(&p.h_recv_rk, std::max<size_t>(1, 2 * nr) * sizeof(int)));
+    }
+  });
+}
+
+int ttdvm_cuda_halo_stats(ttdvm_ctx* c, double* out4) {
+  return guard(c, [&] {
+    require(out4 != nullptr, "halo_stats: null output");
+    out4[0] = (double)c->halo_exchanges;
+    out4[1] = (double)c->halo_bytes_sent;
+    out4[2] = (double)c->halo_bytes_recv;
+    out4[3] = c->halo_ms;
+  });
+}
+
 int ttdvm_cuda_set_owned(ttdvm_ctx* c, int32_t nowned) {
   return guard(c, [&] {
     require(nowned >= 1 && nowned <= c->ncell, "owned cell count out of range");
@@ -2104,7 +2523,7 @@ int ttdvm_cuda_timed_step(ttdvm_ctx* c, double dt, double eps, int32_t cap, int3
     CK(cudaEventCreate(&b));
     CK(cudaStreamSynchronize(c->st));
     CK(cudaEventRecord(a, c->st));
-    for (int k = 0; k < nsteps; ++k) step_once(c, dt, eps, cap);
+    for (int k = 0; k < nsteps; ++k) step_synced(c, dt, eps, cap);
     CK(cudaEventRecord(b, c->st));
     CK(cudaEventSynchronize(b));
     float f = 0.f;

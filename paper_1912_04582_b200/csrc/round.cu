@@ -62,13 +62,59 @@ __device__ __forceinline__ void prefetch_l1(const double* p, long long count) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
 }
 
+// ---- operand cache: TMA bulk copies of whole operand tensors ---------------
+// Every operand (a cell's f, a face flux, J, the xi_n / |xi_n| factor of a
+// face) is one contiguous [first | middle | last] block of its arena, so one
+// cp.async.bulk per distinct operand brings all of an output's inputs into
+// shared memory while the CTA sets up; completion is tracked by an mbarrier
+// (complete_tx).  The phases that follow -- materialising F / last^T, the
+// slice stages of both cuts and of the output -- then read shared memory
+// instead of taking an L2 / HBM round trip each.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  const unsigned a = smem_u32(bar);
+  while (!done) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+
 // Resolve the summands of output o into TermInfo (thread k reads term k;
 // thread 0 then forms the running offsets from shared memory) and the row /
 // column -> term maps.  A term's ranks are (fa1 b1, fa2 b2): the Hadamard
 // product fb o base (proj/src/tt_tensor.cpp:212-245) is never formed, its
 // Kronecker-structured cores are built on the fly where they are consumed.
 __device__ void setup_terms(const RoundArgs& p, int o, TermInfo* terms, int* rowterm,
-                            int* colterm, int* s_meta, int& K, int& R1, int& R2) {
+                            int* colterm, int* s_meta, int& K, int& R1, int& R2,
+                            double* ocbuf = nullptr, int OC = 0,
+                            unsigned long long* ocbar = nullptr) {
   const long long t0 = p.term_off ? p.term_off[o] : (long long)o;
   K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
   const int n1 = p.n1, n2 = p.n2, n3 = p.n3;
@@ -115,6 +161,38 @@ __device__ void setup_terms(const RoundArgs& p, int o, TermInfo* terms, int* row
     }
     s_meta[0] = off1;
     s_meta[1] = off2;
+    if (OC > 0) {
+      // one bulk copy per distinct operand; a term whose operand another
+      // term already fetched (f_L under both xi_n and |xi_n|) shares the copy
+      const double* src[2 * kMaxTerms];
+      double* dst[2 * kMaxTerms];
+      int cnt[2 * kMaxTerms];
+      int nsrc = 0, used = 0;
+      unsigned tx = 0;
+      auto place = [&](const double* g, long long doubles) -> const double* {
+        for (int q = 0; q < nsrc; ++q)
+          if (src[q] == g) return dst[q];
+        // 16-byte aligned source and size (even n always is; else stay on global loads)
+        if ((reinterpret_cast<unsigned long long>(g) & 15ull) || (doubles & 1) ||
+            used + doubles > OC)
+          return g;
+        src[nsrc] = g;
+        dst[nsrc] = ocbuf + used;
+        cnt[nsrc] = (int)doubles;
+        used += (int)doubles;
+        tx += 8u * (unsigned)doubles;
+        return dst[nsrc++];
+      };
+      for (int k = 0; k < K; ++k) {
+        TermInfo& t = terms[k];
+        t.base = place(t.base, (long long)n1 * t.b1 + (long long)n2 * t.b1 * t.b2 + (long long)t.b2 * n3);
+        if (t.fb)
+          t.fb = place(t.fb, (long long)n1 * t.fa1 + (long long)n2 * t.fa1 * t.fa2 + (long long)t.fa2 * n3);
+      }
+      mbar_init(ocbar, 1);
+      mbar_expect_tx(ocbar, tx);
+      for (int q = 0; q < nsrc; ++q) bulk_g2s(dst[q], src[q], 8u * (unsigned)cnt[q], ocbar);
+    }
   }
   __syncthreads();
   R1 = s_meta[0];
@@ -127,13 +205,16 @@ __device__ void setup_terms(const RoundArgs& p, int o, TermInfo* terms, int* row
   // Pull every summand's cores (and Hadamard factor cores) toward L1 now:
   // the slice stages of both cuts and the output read them many phases
   // later, and their loads sit on the critical path of each phase.
+  const double* oc_lo = ocbuf;
+  const double* oc_hi = ocbuf + OC;
   for (int k = 0; k < K; ++k) {
     const TermInfo& t = terms[k];
     const long long nb = (long long)n1 * t.b1 + (long long)n2 * t.b1 * t.b2 + (long long)t.b2 * n3;
-    prefetch_l1(t.base, nb);
-    if (t.fb)
+    if (!(OC > 0 && t.base >= oc_lo && t.base < oc_hi)) prefetch_l1(t.base, nb);
+    if (t.fb && !(OC > 0 && t.fb >= oc_lo && t.fb < oc_hi))
       prefetch_l1(t.fb, (long long)n1 * t.fa1 + (long long)n2 * t.fa1 * t.fa2 + (long long)t.fa2 * n3);
   }
+  if (OC > 0) mbar_wait(ocbar, 0);  // the operands have landed
 }
 
 // F (n1 x R1, ld n1) and last^T (n3 x R2, ld n3) of the implicit sum.
@@ -1103,7 +1184,9 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
   const int JB = SPILL ? 1 : p.JB;
   const GramPlan gp = gram_plan(n1, n3, RM1, RM2, JB);
   const int mx = gp.mx, RMX = gp.RMX, D1 = gp.D1, D3 = gp.D3, D = gp.D;
-  double* cur = sm;
+  const int OC = SPILL ? 0 : p.OC;
+  double* ocbuf = sm;              // OC doubles, 16-byte aligned (operand cache)
+  double* cur = sm + ((OC + 1) & ~1);
   double *F, *lastT, *XP, *G;
   if (SPILL) {
     F = p.gscratch + (long long)blockIdx.x * p.gstride;  // n1 x RMX
@@ -1161,7 +1244,8 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
     }                                                                \
   }
   int K, R1, R2;
-  setup_terms(p, o, terms, rowterm, colterm, s_meta, K, R1, R2);
+  setup_terms(p, o, terms, rowterm, colterm, s_meta, K, R1, R2, ocbuf, OC,
+              reinterpret_cast<unsigned long long*>(s_meta + 8));
   materialise_outer(F, lastT, terms, K, n1, n2, n3);
   __syncthreads();
   PROF(0);
@@ -1502,8 +1586,8 @@ template <int Q, bool SPILL>
 __global__ void __launch_bounds__(NT, SPILL ? 1 : (Q == 0 ? TTDVM_TINY_MINB * 128 / NT : (Q <= 3 ? 512 / NT : (Q <= 10 ? (NT == 128 ? 3 : 1) : 1))))
     round_gram_kernel(RoundArgs p) {
   constexpr int QB = Q == 0 ? 1 : Q;
-  extern __shared__ double sm[];
-  __shared__ int s_meta[8];
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) int s_meta[10];  // [8..9]: the operand cache's mbarrier
   if constexpr (!SPILL) {
     const int o = p.olist ? p.olist[blockIdx.x] : blockIdx.x;
     if (o < p.nout) round_gram_body<QB, false>(p, o, sm, s_meta);
@@ -1612,7 +1696,8 @@ cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st) 
     const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX, 1, true);
     return launch_gram_q<true>(a, nblocks, smem, st, nullptr);
   }
-  const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX, a.JB, false);
+  const size_t smem = round_gram_smem_bytes(a.n1, a.n3, a.RM1, a.RM2, a.MSMAX, a.JB, false) +
+                      8 * (size_t)((a.OC + 1) & ~1);
   return launch_gram_q<false>(a, nblocks, smem, st, nullptr);
 }
 
@@ -1657,14 +1742,25 @@ __global__ void __launch_bounds__(256) round_bin_kernel(RoundArgs p, int* counts
     if (o < p.nout) {
       const long long t0 = p.term_off ? p.term_off[o] : o;
       const int K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
-      int r1 = 0, r2 = 0, ms = 0;
+      int r1 = 0, r2 = 0, ms = 0, oc = 0;
       for (int k = 0; k < K; ++k) {
         const Term tm = p.terms[t0 + k];
         const TSet& s = p.sets[tm.set];
         int a = s.ranks[2 * tm.idx], b = s.ranks[2 * tm.idx + 1];
+        // doubles of the distinct operands (operand cache): an operand that an
+        // earlier summand of this output already names is counted once
+        bool dup = false, fdup = tm.fset < 0;
+        for (int q = 0; q < k; ++q) {
+          const Term tq = p.terms[t0 + q];
+          dup |= tq.set == tm.set && tq.idx == tm.idx;
+          fdup |= tq.fset == tm.fset && tq.fidx == tm.fidx;
+        }
+        if (!dup) oc += p.n1 * a + p.n2 * a * b + b * p.n3;
         if (tm.fset >= 0) {
-          a *= p.sets[tm.fset].ranks[2 * tm.fidx];
-          b *= p.sets[tm.fset].ranks[2 * tm.fidx + 1];
+          const int fa = p.sets[tm.fset].ranks[2 * tm.fidx], fb = p.sets[tm.fset].ranks[2 * tm.fidx + 1];
+          if (!fdup) oc += p.n1 * fa + p.n2 * fa * fb + fb * p.n3;
+          a *= fa;
+          b *= fb;
         }
         r1 += a;
         r2 += b;
@@ -1678,6 +1774,7 @@ __global__ void __launch_bounds__(256) round_bin_kernel(RoundArgs p, int* counts
       atomicMax(&s_max[kBinWords * bin + 1], r2);
       atomicMax(&s_max[kBinWords * bin + 2], ms);
       atomicMax(&s_max[kBinWords * bin + 3], K);
+      atomicMax(&s_max[kBinWords * bin + 4], oc);
     }
     __syncthreads();
     if (threadIdx.x < kRankBins) {

@@ -13,8 +13,8 @@ constexpr int kRoundThreads = 128;
 // rank bins of a rounding launch: upper edges of max(R1, R2) of the summed input
 constexpr int kRankBins = 11;
 // per-bin maxima written by the bin kernel: R1, R2, staged-slice doubles,
-// summands
-constexpr int kBinWords = 4;
+// summands, doubles of the distinct operand tensors (operand cache)
+constexpr int kBinWords = 5;
 __device__ __constant__ const int kRankEdges[kRankBins] = {4, 8, 12, 16, 24, 32, 48, 64, 96, 128,
                                                            1 << 30};
 
@@ -95,6 +95,9 @@ struct RoundArgs {
   int HMAX;                     // rows of the TSQR block buffer
   int MSMAX;                    // doubles of the staged middle slices
   int JB;                       // slices per barrier phase (exact-Gram kernel)
+  int OC;                       // doubles of the shared-memory operand cache (0 = off): every
+                                // distinct operand tensor of an output is fetched whole by one
+                                // cp.async.bulk (TMA) at set-up and read from shared memory after
   // spill plan (working sets above the shared-memory budget: n = 64, large
   // summed ranks): the four largest buffers live in a per-CTA global scratch
   // slice (L1/L2-resident) and the launch is persistent over nblk outputs

@@ -35,7 +35,9 @@ EXPORTS = (
     "ttdvm_cuda_timed_step", "ttdvm_cuda_fp64_peak", "ttdvm_cuda_round_profile",
     "ttdvm_cuda_set_owned", "ttdvm_cuda_set_blocks", "ttdvm_cuda_halo_pack", "ttdvm_cuda_halo_unpack",
     "ttdvm_cuda_face_factors", "ttdvm_cuda_wall_densities", "ttdvm_cuda_setup_info",
-    "ttdvm_cuda_round_resident", "ttdvm_cuda_phase_report",
+    "ttdvm_cuda_round_resident", "ttdvm_cuda_phase_report", "ttdvm_cuda_nccl_unique_id",
+    "ttdvm_cuda_comm_init", "ttdvm_cuda_set_comm", "ttdvm_cuda_set_partition",
+    "ttdvm_cuda_halo_stats",
 )
 
 OK, EINVAL, EDOMAIN, ENOMEM, ECUDA, ENCCL = range(6)
@@ -102,6 +104,11 @@ def load_library(path: str = LIB_PATH):
         "ttdvm_cuda_setup_info": (C.c_int, [vp, vp]),
         "ttdvm_cuda_round_resident": (C.c_int, [vp, dbl, i32, i32, vp]),
         "ttdvm_cuda_phase_report": (C.c_int, [vp, i32, vp, vp, vp, vp]),
+        "ttdvm_cuda_nccl_unique_id": (C.c_int, [vp]),
+        "ttdvm_cuda_comm_init": (C.c_int, [vp, i32, i32, vp]),
+        "ttdvm_cuda_set_comm": (C.c_int, [vp, vp, i32, i32]),
+        "ttdvm_cuda_set_partition": (C.c_int, [vp, i32, i32, vp, vp, vp, vp, vp]),
+        "ttdvm_cuda_halo_stats": (C.c_int, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -239,6 +246,44 @@ class Context:
         """Cells [0, nowned) are stepped; the rest are halo ghosts."""
         self._check(self.lib.ttdvm_cuda_set_owned(self.h, int(nowned)))
         self.nowned = int(nowned)
+
+    # -- in-library NCCL halo exchange (include/ttdvm_cuda.h, multi-GPU section)
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        rc = load_library().ttdvm_cuda_nccl_unique_id(C.cast(buf, C.c_void_p))
+        if rc != OK:
+            raise RuntimeError("libnccl could not be loaded by libttdvm_cuda.so")
+        return buf.raw
+
+    def comm_init(self, nranks: int, rank: int, unique_id: bytes):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self._check(self.lib.ttdvm_cuda_comm_init(self.h, int(nranks), int(rank),
+                                                  C.cast(buf, C.c_void_p)))
+
+    def set_partition(self, n_owned: int, send: dict, recv: dict):
+        """send / recv: peer rank -> local cell ids (LocalPart.send / .recv)."""
+        peers = sorted(set(send) | set(recv))
+        s_off, r_off = np.zeros(len(peers) + 1, np.int64), np.zeros(len(peers) + 1, np.int64)
+        s_ids, r_ids = [], []
+        for k, q in enumerate(peers):
+            a = np.asarray(send.get(q, ()), dtype=np.int32)
+            b = np.asarray(recv.get(q, ()), dtype=np.int32)
+            s_ids.append(a)
+            r_ids.append(b)
+            s_off[k + 1] = s_off[k] + a.size
+            r_off[k + 1] = r_off[k] + b.size
+        cat = lambda v: np.ascontiguousarray(np.concatenate(v) if v else np.zeros(0), dtype=np.int32)  # noqa: E731
+        pr = np.asarray(peers, dtype=np.int32)
+        si, ri = cat(s_ids), cat(r_ids)
+        self._check(self.lib.ttdvm_cuda_set_partition(self.h, int(n_owned), len(peers), _ptr(pr),
+                                                      _ptr(s_off), _ptr(si), _ptr(r_off), _ptr(ri)))
+
+    def halo_stats(self) -> dict:
+        out = np.zeros(4)
+        self._check(self.lib.ttdvm_cuda_halo_stats(self.h, _ptr(out)))
+        return {"exchanges": int(out[0]), "bytes_sent": int(out[1]), "bytes_recv": int(out[2]),
+                "host_ms": float(out[3])}
 
     def halo_pack(self, ids: np.ndarray, dev_ptr: int, capacity: int):
         """Pack current states of local cells `ids` into the device buffer at
