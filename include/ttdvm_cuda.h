@@ -94,6 +94,21 @@ int ttdvm_cuda_download_state(ttdvm_ctx* ctx, double* cores, int64_t capacity);
  * the reference). */
 int ttdvm_cuda_step(ttdvm_ctx* ctx, double dt, double eps, int32_t cap, int32_t nsteps);
 
+/* One LU-SGS implicit iteration, `niter` times (SPEC.md:399-407 lusgs_step;
+ * SURVEY.md §8(f) N4): the explicit residual of ttdvm_cuda_step, then forward
+ * and backward Gauss-Seidel sweeps over the cells in index order with the
+ * first-order upwind Jacobian splitting; the diagonal is the constant rank-1
+ * over-estimate d_i = 1/dt + nu_i + (1/2)(1/V_i) sum_j A_j sqrt(3) xi_box_max,
+ * divided out exactly (TtTensor::divided_by_rank_one,
+ * proj/src/tt_tensor.cpp:247-261); every bracket and the update are rounded
+ * at (eps, cap).  The sweeps run level by level (a cell's level = its longest
+ * chain of lower- / higher-indexed neighbours), each level one batched
+ * rounding launch, which reproduces the natural-order sweep.  Unpartitioned
+ * meshes only. */
+int ttdvm_cuda_lusgs_step(ttdvm_ctx* ctx, double dt, double eps, int32_t cap, int32_t niter);
+/* Levels (= batched launches) of the forward and backward sweeps. */
+int ttdvm_cuda_lusgs_levels(ttdvm_ctx* ctx, int32_t* forward_levels, int32_t* backward_levels);
+
 /* Bounded-memory step: the face fluxes, residuals and updates of a step are
  * formed in `nblocks` contiguous ranges of the owned cells (the fluxes of
  * faces between two blocks are rounded in both), so the flux and residual

@@ -63,6 +63,7 @@ def lib():
             "ttref_set_bcs": (C.c_int, [vp, i32, vp]),
             "ttref_set_state": (C.c_int, [vp, vp]),
             "ttref_step": (C.c_int, [vp, dbl, dbl, i32, i32, vp]),
+            "ttref_lusgs_step": (C.c_int, [vp, dbl, dbl, i32]),
             "ttref_times": (C.c_int, [vp, vp]),
             "ttref_layout": (C.c_int, [vp, i32, vp, vp, vp]),
             "ttref_download": (C.c_int, [vp, i32, vp]),
@@ -164,6 +165,10 @@ class RefSolver:
         else:
             c = np.ascontiguousarray(cells, dtype=np.int32)
             self._check(self.L.ttref_step(self.h, dt, eps, cap, len(c), _ptr(c)))
+
+    def lusgs_step(self, dt: float, eps: float, cap: int = 0):
+        """One LU-SGS iteration over every cell (oracle/ref_step.cpp lusgs)."""
+        self._check(self.L.ttref_lusgs_step(self.h, dt, eps, cap))
 
     def times(self):
         t = np.zeros(2)

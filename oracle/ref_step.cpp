@@ -284,6 +284,78 @@ void step(ttref_solver* s, double dt, double eps, int cap, const std::vector<int
   s->step_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// One LU-SGS iteration from reference API calls only:
+// the composition of SPEC.md:399-407 that oracle/step.py lusgs_step documents
+// -- the explicit residual of S1, forward and backward Gauss-Seidel sweeps in
+// cell index order with the first-order upwind Jacobian splitting, the
+// diagonal replaced by the constant rank-1 over-estimate and divided out by
+// TtTensor::divided_by_rank_one (tt_tensor.cpp:247-261).  Sequential sweeps
+// (SPEC.md "Concurrency Model"); fluxes and residuals in parallel.
+void lusgs(ttref_solver* s, double dt, double eps, int cap) {
+  if ((int)s->f.size() != s->ncell) throw std::invalid_argument("state count must equal the cell count");
+  std::vector<int> faces(s->nface);
+  for (int j = 0; j < s->nface; ++j) faces[j] = j;
+  warm_factors(s, faces);
+  const int nc = s->ncell, n = s->nv;
+  s->phi.assign(s->nface, TtTensor());
+#pragma omp parallel for schedule(dynamic, 8) num_threads(s->nthreads)
+  for (int j = 0; j < s->nface; ++j) s->phi[j] = face_flux(s, j, eps, cap);
+  std::vector<TtTensor> res(nc);
+  std::vector<double> diag(nc);
+  s->macros.assign(11 * (size_t)nc, 0.0);
+  const double xi_abs_max = std::sqrt(3.0) * s->bound;
+#pragma omp parallel for schedule(dynamic, 4) num_threads(s->nthreads)
+  for (int i = 0; i < nc; ++i) {
+    ttdvm::Macroparameters m;
+    TtTensor acc = ttdvm::compute_collision(s->f[i], main_grid(s), s->gas, eps, m);
+    double sa = 0.0;
+    for (long long e = s->cfo[i]; e < s->cfo[i + 1]; ++e) {
+      const int fid = s->cfid[e];
+      acc = acc + s->phi[fid].scaled(-s->cfs[e] * s->area[fid] / s->volume[i]);
+      sa += s->area[fid];
+    }
+    res[i] = acc.rounded(eps, cap);
+    const double nu = m.pressure / ttdvm::viscosity(m.temperature, s->gas);
+    diag[i] = 1.0 / dt + nu + 0.5 * sa * xi_abs_max / s->volume[i];
+    double* o = &s->macros[11 * (size_t)i];
+    o[0] = m.number_density;
+    for (int a = 0; a < 3; ++a) o[1 + a] = m.velocity(a);
+    o[4] = m.temperature;
+    o[5] = m.mass_density;
+    o[6] = m.pressure;
+    for (int a = 0; a < 3; ++a) o[7 + a] = m.shakhov_s(a);
+    o[10] = nu;
+  }
+  const Eigen::VectorXd ones = Eigen::VectorXd::Ones(n);
+  auto bracket = [&](int i, TtTensor acc, bool lower, const std::vector<TtTensor>& d) {
+    for (long long e = s->cfo[i]; e < s->cfo[i + 1]; ++e) {
+      const int fid = s->cfid[e];
+      const int l = s->left[fid], r = s->right[fid];
+      if (r < 0) continue;
+      const int k = l == i ? r : l;
+      if (lower ? !(k < i) : !(k > i)) continue;
+      const Factors& fa = s->factors.at(normal_key(s->normal[fid]));
+      const double w = s->area[fid] / s->volume[i];
+      acc = acc + (l == i ? ttdvm::hadamard(fa.xm, d[k]).scaled(-w) : ttdvm::hadamard(fa.xp, d[k]).scaled(w));
+    }
+    return acc.rounded(eps, cap);
+  };
+  std::vector<TtTensor> bstar(nc), dstar(nc), delta(nc);
+  for (int i = 0; i < nc; ++i) {
+    bstar[i] = bracket(i, res[i], true, dstar);
+    dstar[i] = bstar[i].divided_by_rank_one(diag[i] * ones, ones, ones);
+  }
+  for (int i = nc - 1; i >= 0; --i)
+    delta[i] = bracket(i, bstar[i], false, delta).divided_by_rank_one(diag[i] * ones, ones, ones);
+  std::vector<TtTensor> fnew(nc);
+#pragma omp parallel for schedule(dynamic, 4) num_threads(s->nthreads)
+  for (int i = 0; i < nc; ++i) fnew[i] = (s->f[i] + delta[i]).rounded(eps, cap);
+  s->f = std::move(fnew);
+  s->res = std::move(res);
+  s->last_cells.resize(nc);
+  for (int i = 0; i < nc; ++i) s->last_cells[i] = i;
+}
+
 std::vector<TtTensor> unpack_all(const ttref_batch* b) {
   if (!b || b->count < 0) throw std::invalid_argument("null batch");
   std::vector<TtTensor> v(b->count);
@@ -381,6 +453,10 @@ int ttref_step(ttref_solver* s, double dt, double eps, int32_t cap, int32_t ncel
       for (int i = 0; i < s->ncell; ++i) sel.push_back(i);
     step(s, dt, eps, cap, sel);
   });
+}
+
+int ttref_lusgs_step(ttref_solver* s, double dt, double eps, int32_t cap) {
+  return guard(s, [&] { lusgs(s, dt, eps, cap); });
 }
 
 int ttref_times(ttref_solver* s, double* step_s_and_factor_s) {

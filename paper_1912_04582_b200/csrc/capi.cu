@@ -67,6 +67,9 @@ struct MacroArgs {
 cudaError_t launch_macro(const MacroArgs& a, int rmax, cudaStream_t st);
 cudaError_t launch_shakhov_raw(const double* macro, int count, int n, const double* nodes,
                                double R, double prandtl, double* out, cudaStream_t st);
+cudaError_t launch_lusgs_diag(const double* nu, const double* geom, double inv_dt, int count,
+                              const int* pos_f, const int* pos_b, double* diag, double* inv_f,
+                              double* inv_b, cudaStream_t st);
 cudaError_t launch_gather(const TSet& s, int count, const long long* dst_off, int n1, int n2,
                           int n3, double* dst, cudaStream_t st);
 struct FaceFactorArgs {
@@ -258,6 +261,8 @@ enum SetId {
   S_IN = 7,
   S_XIN = 8,   // exact rank-2 xi_n per oblique normal
   S_EABS = 9,  // |xi_n| estimate per oblique normal
+  S_DSTAR = 10,  // LU-SGS forward increments (brackets B*, per-tensor scale 1/d), sweep order
+  S_DELTA = 11,  // LU-SGS backward increments (brackets B, per-tensor scale 1/d), sweep order
 };
 
 struct TermList {
@@ -325,6 +330,17 @@ struct ttdvm_ctx {
   std::vector<double> factors;
   DevBuf<double> d_factors;
   TermList t_fs, t_col, t_flux, t_res, t_upd, t_batch;
+  // LU-SGS (N4): per-face factor ids kept from build_step_terms, the level
+  // schedules of the two sweeps and their summand lists
+  std::vector<int> facp, facm, nid;
+  bool lusgs_built = false;
+  std::vector<int> lev_off_f, lev_off_b;   // outputs of level l: [lev_off[l], lev_off[l+1])
+  std::vector<int> pos_f, pos_b;           // cell -> position in the sweep order
+  TermList t_lf, t_lb, t_lu;
+  TensorSet dstar, delta;
+  DevBuf<int> d_pos_f, d_pos_b;
+  DevBuf<double> d_lgeom, d_ldiag, d_linv_f, d_linv_b;
+  const double* dscale_override = nullptr;  // RoundArgs::dscale of the LU-SGS launches
   // blocked step (bounded memory): owned cells in nblocks contiguous ranges,
   // each with its own flux (faces it touches), residual and update lists
   int nblocks = 1;           // blocks in use
@@ -526,8 +542,10 @@ void grow_preserve(ttdvm_ctx* c, TensorSet& s, long long keep, long long need);
 // blocked step): output o becomes entry obase + o of `out` (sized by the
 // caller) and is placed after the `out.used` doubles already in its arena.
 void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets], TensorSet& out,
-               double eps, int cap, double* margins_dev, long long obase = -1) {
-  const int nout = tl.nout();
+               double eps, int cap, double* margins_dev, long long obase = -1, int first = 0,
+               int count = -1) {
+  // (first, count): round only outputs [first, first + count) of the list
+  const int nout = count >= 0 ? count : tl.nout();
   const bool append = obase >= 0;
   if (!append) out.resize(nout);
   if (nout == 0) return;
@@ -538,10 +556,10 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   memset(&a, 0, sizeof(a));
   for (int s = 0; s < kMaxSets; ++s)
     if (sets[s]) a.sets[s] = sets[s]->view();
-  a.term_off = tl.d_off.p;
+  a.term_off = tl.d_off.p + first;
   a.terms = tl.d_terms.p;
   a.factors = c->d_factors.p;
-  a.dscale = c->d_nw.p;
+  a.dscale = c->dscale_override ? c->dscale_override : c->d_nw.p;
   a.n1 = a.n2 = a.n3 = n;
   a.nout = nout;
   a.eps = eps;
@@ -550,6 +568,11 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
   a.margins = margins_dev;
   a.acc = c->d_acc.p;
   a.prof = c->round_prof ? c->d_prof.p : nullptr;
+  static const bool no_dmma = [] {  // A/B: TTDVM_DMMA=0 keeps every slice product on DFMA
+    const char* e = getenv("TTDVM_DMMA");
+    return e && *e == '0';
+  }();
+  a.no_dmma = no_dmma ? 1 : 0;
   // rank bins: per-bin shared-memory plans (one tiny kernel + readback)
   constexpr int kBinAll = kRankBins * (1 + kBinWords);
   c->d_bins.alloc((size_t)kBinAll);
@@ -718,6 +741,9 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     }
   }
   for (int attempt = 0; attempt < 4; ++attempt) {
+    // (the output arena may have moved; a sweep reads the set it appends to)
+    for (int s = 0; s < kMaxSets; ++s)
+      if (sets[s]) a.sets[s] = sets[s]->view();
     a.out.ranks = out.ranks.p + (append ? 2 * obase : 0);
     a.out.off = out.off.p + (append ? obase : 0);
     a.out.base = out.arena.p;
@@ -1224,7 +1250,11 @@ void build_step_terms(ttdvm_ctx* c) {
   // axis normals, proj/tests/test_velocity_grid.cpp:98-115); oblique
   // normals: xi_n and E per distinct normal, computed on the device.
   c->factors.clear();
-  std::vector<int> facp(c->nface, -1), facm(c->nface, -1), nid(c->nface, -1);
+  std::vector<int>&facp = c->facp, &facm = c->facm, &nid = c->nid;
+  facp.assign(c->nface, -1);
+  facm.assign(c->nface, -1);
+  nid.assign(c->nface, -1);
+  c->lusgs_built = false;
   int pair_id[6];
   for (int k = 0; k < 6; ++k) pair_id[k] = -1;
   struct KeyHash {
@@ -1839,6 +1869,178 @@ void step_once(ttdvm_ctx* c, double dt, double eps, int cap) {
   c->cur = 1 - c->cur;
 }
 
+
+// ---------------------------------------------------------------------------
+// LU-SGS implicit iteration (the
+// rank-1 divisor of TtTensor::divided_by_rank_one, tt_tensor.cpp:247-261).
+// The reference's sweeps run over the cells in index order; here a cell's
+// LEVEL is the length of its longest chain of lower-indexed (forward) or
+// higher-indexed (backward) neighbours, and each level is one batched
+// rounding launch: every cell sees exactly the neighbour increments the
+// sequential sweep would give it and sums them in the same (face) order, so
+// the result is that of the natural-order sweep.
+void build_lusgs_terms(ttdvm_ctx* c) {
+  if (c->lusgs_built) return;
+  const int nc = c->ncell;
+  auto neighbour = [&](int i, int fid) {
+    const int l = c->left[fid], r = c->right[fid];
+    return r < 0 ? -1 : (l == i ? r : l);
+  };
+  // level schedules
+  std::vector<int> lev(nc, 0);
+  auto schedule = [&](bool forward, std::vector<int>& lev_off, std::vector<int>& pos) {
+    std::fill(lev.begin(), lev.end(), 0);
+    int nlev = 0;
+    for (int q = 0; q < nc; ++q) {
+      const int i = forward ? q : nc - 1 - q;
+      int l = 0;
+      for (long long e = c->cfo[i]; e < c->cfo[i + 1]; ++e) {
+        const int k = neighbour(i, c->cfid[e]);
+        if (k >= 0 && (forward ? k < i : k > i)) l = std::max(l, lev[k] + 1);
+      }
+      lev[i] = l;
+      nlev = std::max(nlev, l + 1);
+    }
+    lev_off.assign(nlev + 1, 0);
+    for (int i = 0; i < nc; ++i) lev_off[lev[i] + 1] += 1;
+    for (int l = 0; l < nlev; ++l) lev_off[l + 1] += lev_off[l];
+    std::vector<int> fill(lev_off.begin(), lev_off.end() - 1);
+    pos.assign(nc, 0);
+    for (int i = 0; i < nc; ++i) pos[i] = fill[lev[i]]++;  // ascending cell id inside a level
+  };
+  schedule(true, c->lev_off_f, c->pos_f);
+  schedule(false, c->lev_off_b, c->pos_b);
+  std::vector<int> order_f(nc), order_b(nc);
+  for (int i = 0; i < nc; ++i) {
+    order_f[c->pos_f[i]] = i;
+    order_b[c->pos_b[i]] = i;
+  }
+  // -c_ik o d_k: i left of the face: -(A/V) xm o d_k; i right: +(A/V) xp o d_k
+  auto push_offdiag = [&](TermList& tl, int i, int fid, int set, int kpos) {
+    const bool is_left = c->left[fid] == i;
+    const double w = c->area[fid] / c->volume[i];
+    const double sc = is_left ? -w : w;
+    Term t{set, kpos, sc};
+    if (c->nid[fid] < 0) {
+      t.fac = is_left ? c->facm[fid] : c->facp[fid];
+      tl.terms.push_back(t);
+    } else {
+      t.fidx = c->nid[fid];
+      t.fset = S_XIN;
+      t.scale = 0.5 * sc;
+      tl.terms.push_back(t);
+      t.fset = S_EABS;
+      t.scale = (is_left ? -0.5 : 0.5) * sc;  // xm = (xi_n - E)/2, xp = (xi_n + E)/2
+      tl.terms.push_back(t);
+    }
+  };
+  TermList &lf = c->t_lf, &lb = c->t_lb, &lu = c->t_lu;
+  lf.off.assign(1, 0);
+  lf.terms.clear();
+  lb.off.assign(1, 0);
+  lb.terms.clear();
+  for (int o = 0; o < nc; ++o) {
+    const int i = order_f[o];
+    lf.terms.push_back(Term{S_RES, i, 1.0});
+    for (long long e = c->cfo[i]; e < c->cfo[i + 1]; ++e) {
+      const int k = neighbour(i, c->cfid[e]);
+      if (k >= 0 && k < i) push_offdiag(lf, i, c->cfid[e], S_DSTAR, c->pos_f[k]);
+    }
+    lf.off.push_back((long long)lf.terms.size());
+  }
+  for (int o = 0; o < nc; ++o) {
+    const int i = order_b[o];
+    Term bs{S_DSTAR, c->pos_f[i], 1.0};
+    bs.dsi = i;  // x d_i: the undivided forward bracket B*_i
+    lb.terms.push_back(bs);
+    for (long long e = c->cfo[i]; e < c->cfo[i + 1]; ++e) {
+      const int k = neighbour(i, c->cfid[e]);
+      if (k >= 0 && k > i) push_offdiag(lb, i, c->cfid[e], S_DELTA, c->pos_b[k]);
+    }
+    lb.off.push_back((long long)lb.terms.size());
+  }
+  lu.off.resize(nc + 1);
+  lu.terms.resize(2 * (size_t)nc);
+  for (int i = 0; i <= nc; ++i) lu.off[i] = 2LL * i;
+  for (int i = 0; i < nc; ++i) {
+    lu.terms[2 * i] = Term{S_STATE, i, 1.0};
+    lu.terms[2 * i + 1] = Term{S_DELTA, c->pos_b[i], 1.0};
+  }
+  lf.upload();
+  lb.upload();
+  lu.upload();
+  require(std::max(lf.maxk, lb.maxk) <= kMaxTerms, "LU-SGS: too many faces per cell");
+  // geometric part of the diagonal
+  std::vector<double> geom(nc);
+  const double xi_abs_max = std::sqrt(3.0) * c->bound;
+  for (int i = 0; i < nc; ++i) {
+    double sa = 0.0;
+    for (long long e = c->cfo[i]; e < c->cfo[i + 1]; ++e) sa += c->area[c->cfid[e]];
+    geom[i] = 0.5 * sa * xi_abs_max / c->volume[i];
+  }
+  c->d_lgeom.alloc(nc);
+  c->d_ldiag.alloc(nc);
+  c->d_linv_f.alloc(nc);
+  c->d_linv_b.alloc(nc);
+  c->d_pos_f.alloc(nc);
+  c->d_pos_b.alloc(nc);
+  CK(cudaMemcpy(c->d_lgeom.p, geom.data(), 8LL * nc, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_pos_f.p, c->pos_f.data(), 4LL * nc, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_pos_b.p, c->pos_b.data(), 4LL * nc, cudaMemcpyHostToDevice));
+  c->lusgs_built = true;
+}
+
+void lusgs_once(ttdvm_ctx* c, double dt, double eps, int cap) {
+  require(c->nowned < 0 || c->nowned == c->ncell, "LU-SGS runs on an unpartitioned mesh");
+  TensorSet& s = c->state[c->cur];
+  TensorSet& nxt = c->state[1 - c->cur];
+  const int nc = c->ncell;
+  build_lusgs_terms(c);
+  run_collision(c, s, eps, nc);
+  c->jr.tscale = c->d_nu.p;
+  TensorSet* sets[kMaxSets] = {&s,      &c->fsraw,      &c->fs, &c->jr,  &c->phi,  &c->res,
+                                &c->freestream, &c->in, &c->xin, &c->eabs, &c->dstar, &c->delta};
+  if (c->nwall) {
+    Timer t(c, 8);
+    run_walls(c, s, 0);
+  }
+  {
+    Timer t(c, 4);
+    run_round(c, c->t_flux, sets, c->phi, eps, cap, nullptr);
+  }
+  c->res.uscale = 1.0;
+  {
+    Timer t(c, 5);
+    run_round(c, c->t_res, sets, c->res, eps, cap, nullptr);
+  }
+  CK(launch_lusgs_diag(c->d_nu.p, c->d_lgeom.p, 1.0 / dt, nc, c->d_pos_f.p, c->d_pos_b.p,
+                       c->d_ldiag.p, c->d_linv_f.p, c->d_linv_b.p, c->st));
+  c->launches += 1;
+  c->dscale_override = c->d_ldiag.p;
+  try {
+    Timer t(c, 6);
+    for (int pass = 0; pass < 2; ++pass) {
+      TensorSet& out = pass == 0 ? c->dstar : c->delta;
+      const TermList& tl = pass == 0 ? c->t_lf : c->t_lb;
+      const std::vector<int>& lo = pass == 0 ? c->lev_off_f : c->lev_off_b;
+      out.resize(nc);
+      out.used = 0;
+      out.maxr1 = out.maxr2 = 1;
+      out.tscale = pass == 0 ? c->d_linv_f.p : c->d_linv_b.p;
+      for (size_t l = 0; l + 1 < lo.size(); ++l)
+        run_round(c, tl, sets, out, eps, cap, nullptr, lo[l], lo[l], lo[l + 1] - lo[l]);
+    }
+    nxt.resize(nc);
+    run_round(c, c->t_lu, sets, nxt, eps, cap, nullptr);
+  } catch (...) {
+    c->dscale_override = nullptr;
+    throw;
+  }
+  c->dscale_override = nullptr;
+  nxt.count = nc;
+  c->cur = 1 - c->cur;
+}
+
 // One step; with a communicator, every rank learns of a failure on any rank
 // (ncclAllReduce max of the status code) and fails with it.
 void step_synced(ttdvm_ctx* c, double dt, double eps, int cap) {
@@ -1953,7 +2155,14 @@ int ttdvm_cuda_destroy(ttdvm_ctx* c) {
   for (TensorSet* s : {&c->state[0], &c->state[1], &c->fsraw, &c->fs, &c->jr, &c->phi, &c->res,
                        &c->freestream, &c->in, &c->result, &c->xin, &c->eabs})
     s->free();
-  for (TermList* t : {&c->t_fs, &c->t_col, &c->t_flux, &c->t_res, &c->t_upd, &c->t_batch}) t->free();
+  for (TermList* t : {&c->t_fs, &c->t_col, &c->t_flux, &c->t_res, &c->t_upd, &c->t_batch, &c->t_lf,
+                      &c->t_lb, &c->t_lu})
+    t->free();
+  c->dstar.free();
+  c->delta.free();
+  c->d_pos_f.free();
+  c->d_pos_b.free();
+  for (DevBuf<double>* b : {&c->d_lgeom, &c->d_ldiag, &c->d_linv_f, &c->d_linv_b}) b->free();
   for (auto* v : {&c->bt_flux, &c->bt_res, &c->bt_upd})
     for (TermList& t : *v) t.free();
   c->d_gscratch.free();
@@ -2097,6 +2306,28 @@ int ttdvm_cuda_step(ttdvm_ctx* c, double dt, double eps, int32_t cap, int32_t ns
     build_step_terms(c);
     reset_counters(c);
     for (int k = 0; k < nsteps; ++k) step_synced(c, dt, eps, cap);
+  });
+}
+
+int ttdvm_cuda_lusgs_step(ttdvm_ctx* c, double dt, double eps, int32_t cap, int32_t niter) {
+  return guard(c, [&] {
+    require(eps > 0.0, "rounded: eps must be > 0");
+    require(dt > 0.0, "lusgs_step: dt must be > 0");
+    require(c->state[c->cur].count == c->ncell, "state count must equal the mesh cell count");
+    require(c->comm == nullptr, "LU-SGS runs on an unpartitioned mesh");
+    cudaSetDevice(c->device);
+    build_step_terms(c);
+    reset_counters(c);
+    for (int k = 0; k < niter; ++k) lusgs_once(c, dt, eps, cap);
+  });
+}
+
+int ttdvm_cuda_lusgs_levels(ttdvm_ctx* c, int32_t* forward_levels, int32_t* backward_levels) {
+  return guard(c, [&] {
+    build_step_terms(c);
+    build_lusgs_terms(c);
+    if (forward_levels) *forward_levels = (int)c->lev_off_f.size() - 1;
+    if (backward_levels) *backward_levels = (int)c->lev_off_b.size() - 1;
   });
 }
 

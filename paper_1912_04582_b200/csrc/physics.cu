@@ -250,6 +250,32 @@ cudaError_t launch_shakhov_raw(const double* macro, int count, int n, const doub
   return cudaGetLastError();
 }
 
+// LU-SGS diagonal (the constant rank-1 over-estimate):
+// d_i = 1/dt + nu_i + geom_i, geom_i = (1/2)(1/V_i) sum_j A_j sqrt(3) xi_box_max.
+// Written in cell order (the per-term scale of the backward bracket) and,
+// inverted, in the forward / backward sweep orders (the per-tensor scales
+// of the increment sets).
+__global__ void lusgs_diag_kernel(const double* nu, const double* geom, double inv_dt, int count,
+                                  const int* pos_f, const int* pos_b, double* diag,
+                                  double* inv_f, double* inv_b) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double d = inv_dt + nu[i] + geom[i];
+  diag[i] = d;
+  const double r = 1.0 / d;
+  inv_f[pos_f[i]] = r;
+  inv_b[pos_b[i]] = r;
+}
+
+cudaError_t launch_lusgs_diag(const double* nu, const double* geom, double inv_dt, int count,
+                              const int* pos_f, const int* pos_b, double* diag, double* inv_f,
+                              double* inv_b, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  lusgs_diag_kernel<<<(count + 255) / 256, 256, 0, st>>>(nu, geom, inv_dt, count, pos_f, pos_b,
+                                                         diag, inv_f, inv_b);
+  return cudaGetLastError();
+}
+
 // Gather tensors of a set into cell order (download / halo packing).
 __global__ void gather_kernel(TSet s, int count, const long long* dst_off, int n1, int n2, int n3,
                               double* dst) {

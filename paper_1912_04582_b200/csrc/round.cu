@@ -625,12 +625,146 @@ __device__ void stage_slice(double* Ms, const TermInfo* terms, int K, int n1, in
   }
 }
 
+
+// ---- FP64 tensor-core (DMMA) slice products --------------------------------
+// The dense products of the T route and of the high-rank bins (config 3:
+// 32 x 72 x 32 per slice; config 5 residuals and the disturbed faces of
+// config 4: 44..64 x ~100 x 44..64) run on mma.sync.m8n8k4.f64: each warp
+// owns 16 x 16 output super-tiles (2 x 2 register-blocked 8 x 8 tiles, four
+// DMMAs per four fragment loads), so a multiply-add costs 1/16 shared-memory
+// load instead of the 5/4 of the 4-row FMA strips below -- those ran
+// shared-memory-bound at ~6 % of the FP64 peak.  Products are IEEE FMAs
+// (same per-term rounding as DFMA; the k order inside a dot product differs).
+// The exact double-double Gram accumulation stays on DFMA.
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// C(i, j) = sum_{k in [kb(j0), ke(j0))} A(i, k) B(k, j) for i < M, j < N over
+// `nbatch` independent problems (slices); a(q, i, k), b(q, k, j) return 0
+// outside their operand, cst(q, i, j, v) stores inside bounds.  krange(j0,
+// kb, ke) narrows the k loop of a 16-column super-tile (block-diagonal or
+// triangular B).  Every warp of the CTA must call this (mma.sync).
+template <class FA, class FB, class FC, class FK>
+__device__ __forceinline__ void dmma_gemm(int nbatch, int M, int N, FA&& a, FB&& b, FC&& cst,
+                                          FK&& krange) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gr = lane >> 2, gc = lane & 3;
+  const int sm_ = (M + 15) >> 4, sn_ = (N + 15) >> 4;
+  const int per = sm_ * sn_;
+  for (int s = warp; s < nbatch * per; s += NW) {
+    const int q = s / per, t = s - q * per;
+    const int j0 = (t / sm_) << 4, i0 = (t - (t / sm_) * sm_) << 4;
+    int kb, ke;
+    krange(j0, kb, ke);
+    double c00[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c11[2] = {0.0, 0.0};
+    const bool two_i = i0 + 8 < M, two_j = j0 + 8 < N;
+    // two k-steps per iteration: eight fragment loads issued before the
+    // eight DMMAs that consume them (a and b return 0 past their operand /
+    // outside the block, so running up to 4 past ke adds zeros)
+#pragma unroll 2
+    for (int k0 = kb; k0 < ke; k0 += 8) {
+      const int k1 = k0 + 4;
+      const double a0 = a(q, i0 + gr, k0 + gc), a0n = a(q, i0 + gr, k1 + gc);
+      const double b0 = b(q, k0 + gc, j0 + gr), b0n = b(q, k1 + gc, j0 + gr);
+      double a1 = 0.0, a1n = 0.0, b1 = 0.0, b1n = 0.0;
+      if (two_i) {
+        a1 = a(q, i0 + 8 + gr, k0 + gc);
+        a1n = a(q, i0 + 8 + gr, k1 + gc);
+      }
+      if (two_j) {
+        b1 = b(q, k0 + gc, j0 + 8 + gr);
+        b1n = b(q, k1 + gc, j0 + 8 + gr);
+      }
+      dmma884(c00, a0, b0);
+      if (two_j) dmma884(c01, a0, b1);
+      if (two_i) dmma884(c10, a1, b0);
+      if (two_i && two_j) dmma884(c11, a1, b1);
+      dmma884(c00, a0n, b0n);
+      if (two_j) dmma884(c01, a0n, b1n);
+      if (two_i) dmma884(c10, a1n, b0n);
+      if (two_i && two_j) dmma884(c11, a1n, b1n);
+    }
+    const int r = i0 + gr, cc = j0 + 2 * gc;
+    cst(q, r, cc, c00[0]);
+    cst(q, r, cc + 1, c00[1]);
+    if (two_j) {
+      cst(q, r, cc + 8, c01[0]);
+      cst(q, r, cc + 9, c01[1]);
+    }
+    if (two_i) {
+      cst(q, r + 8, cc, c10[0]);
+      cst(q, r + 8, cc + 1, c10[1]);
+      if (two_j) {
+        cst(q, r + 8, cc + 8, c11[0]);
+        cst(q, r + 8, cc + 9, c11[1]);
+      }
+    }
+  }
+}
+
+// Products worth the tensor cores: at least a full 8 x 8 tile in every
+// dimension (the bulk low-rank bins keep the FMA strips).
+__device__ __forceinline__ bool dmma_worth(int M, int N, int K) {
+  return M >= 8 && N >= 8 && K >= 8;
+}
+
+// X_q (rows x R2, ld ldx, batch stride xs) = L (rows x R1, ld ldl) blockdiag(Ms_q):
+// the k range of a column super-tile is the row range of the summands it meets.
+__device__ void dmma_left_times_blockdiag(double* X, int ldx, int xs, const double* L, int ldl,
+                                          int rows, int R1, int R2, const double* Ms, int msld,
+                                          const TermInfo* terms, const int* colterm, int jn) {
+  dmma_gemm(
+      jn, rows, R2,
+      [&](int, int i, int k) { return (i < rows && k < R1) ? L[i + ldl * k] : 0.0; },
+      [&](int q, int k, int j) {
+        if (j >= R2 || k >= R1) return 0.0;
+        const TermInfo& t = terms[colterm[j]];
+        const int a = k - t.off1;
+        return (a >= 0 && a < t.r1) ? Ms[q * msld + t.ms + a + t.r1 * (j - t.off2)] : 0.0;
+      },
+      [&](int q, int i, int j, double v) {
+        if (i < rows && j < R2) X[q * xs + i + ldx * j] = v;
+      },
+      [&](int j0, int& kb, int& ke) {
+        const TermInfo& lo = terms[colterm[min(j0, R2 - 1)]];
+        const TermInfo& hi = terms[colterm[min(j0 + 15, R2 - 1)]];
+        kb = lo.off1 & ~3;
+        ke = hi.off1 + hi.r1;
+      });
+}
+
+// out_q(r, c) = sum_{b >= c} X_q(r, b) R3(c, b), R3 upper trapezoidal in
+// lastT (ld n3; below the diagonal it holds reflectors, masked here);
+// stored at out[q * os + (trans ? c + ldo * r : r + ldo * c)].
+__device__ void dmma_times_r3t(double* out, int ldo, int os, bool trans, const double* X, int ldx,
+                               int xs, int rows, int ncol, int R2, const double* lastT, int n3,
+                               int jn) {
+  dmma_gemm(
+      jn, rows, ncol,
+      [&](int q, int i, int k) { return (i < rows && k < R2) ? X[q * xs + i + ldx * k] : 0.0; },
+      [&](int, int k, int j) { return (j < ncol && k < R2 && k >= j) ? lastT[j + n3 * k] : 0.0; },
+      [&](int q, int i, int j, double v) {
+        if (i < rows && j < ncol) out[q * os + (trans ? j + ldo * i : i + ldo * j)] = v;
+      },
+      [&](int j0, int& kb, int& ke) {
+        kb = j0 & ~3;
+        ke = R2;
+      });
+}
+
 // X (rows x R2, ld ldxp) = L (rows x R1, ld ldl) blockdiag(Ms_t); each
 // thread computes a 4-row strip of one column (4 independent FMA chains,
 // one broadcast Ms load per 4 FMAs).
 __device__ void left_times_blockdiag(double* X, int ldxp, const double* L, int ldl, int rows,
                                      int R2, const double* Ms, const TermInfo* terms,
-                                     const int* colterm) {
+                                     const int* colterm, int R1 = 0) {
+  if (R1 > 0 && dmma_worth(rows, R2, R1)) {
+    dmma_left_times_blockdiag(X, ldxp, 0, L, ldl, rows, R1, R2, Ms, 0, terms, colterm, 1);
+    return;
+  }
   const int ngr = (rows + 3) >> 2;
   for2d(ngr, R2, [&](int ig, int col) {
     const int i0 = ig << 2;
@@ -672,7 +806,11 @@ __device__ void left_times_blockdiag(double* X, int ldxp, const double* L, int l
 // R3 upper trapezoidal in lastT (ld n3); out index r + ldo*c, or c + ldo*r
 // when trans.  4-row strips per thread.
 __device__ void times_r3t(double* out, int ldo, bool trans, const double* X, int ldxp, int rows,
-                          int ncol, int R2, const double* lastT, int n3) {
+                          int ncol, int R2, const double* lastT, int n3, bool tensor = false) {
+  if (tensor && dmma_worth(rows, ncol, R2)) {
+    dmma_times_r3t(out, ldo, 0, trans, X, ldxp, 0, rows, ncol, R2, lastT, n3, 1);
+    return;
+  }
   const int ngr = (rows + 3) >> 2;
   for2d(ngr, ncol, [&](int ig, int c) {
     const int r0 = ig << 2;
@@ -750,7 +888,12 @@ __device__ void stage_slices(double* Ms, int msld, const TermInfo* terms, int K,
 // X_jj (rows x R2, ld ldx, slice stride xs) = L (rows x R1, ld ldl) blockdiag(Ms_jj)
 __device__ void left_times_blockdiag_b(double* X, int ldx, int xs, const double* L, int ldl,
                                        int rows, int R2, const double* Ms, int msld,
-                                       const TermInfo* terms, const int* colterm, int jn) {
+                                       const TermInfo* terms, const int* colterm, int jn,
+                                       int R1 = 0) {
+  if (R1 > 0 && dmma_worth(rows, R2, R1)) {
+    dmma_left_times_blockdiag(X, ldx, xs, L, ldl, rows, R1, R2, Ms, msld, terms, colterm, jn);
+    return;
+  }
   const int ngr = (rows + 3) >> 2;
   for2d(ngr, jn * R2, [&](int ig, int jc) {
     const int jj = jc / R2, col = jc - jj * R2;
@@ -778,7 +921,12 @@ __device__ void left_times_blockdiag_b(double* X, int ldx, int xs, const double*
 // out_jj(c, r) = sum_{b >= c} X_jj(r, b) R3(c, b) (transposed, ld ldo, slice
 // stride os) for r < rows, c < ncol; X_jj at X + jj * xs (ld ldx)
 __device__ void times_r3t_b(double* out, int ldo, int os, const double* X, int ldx, int xs,
-                            int rows, int ncol, int R2, const double* lastT, int n3, int jn) {
+                            int rows, int ncol, int R2, const double* lastT, int n3, int jn,
+                            bool tensor = false) {
+  if (tensor && dmma_worth(rows, ncol, R2)) {
+    dmma_times_r3t(out, ldo, os, true, X, ldx, xs, rows, ncol, R2, lastT, n3, jn);
+    return;
+  }
   const int ngr = (rows + 3) >> 2;
   for2d(ngr, jn * ncol, [&](int ig, int jc) {
     const int jj = jc / ncol, c = jc - jj * ncol;
@@ -803,9 +951,12 @@ __device__ void times_r3t_b(double* out, int ldo, int os, const double* X, int l
 
 // Block or single-warp pivoted dd Cholesky / svd_from_r by size; results
 // (rank, truncation) broadcast to the CTA through s_int.
+template <bool LEAN = false>
 __device__ __forceinline__ int chol_any(double* Gh, double* Gl, int d, double thresh, double* R,
                                         int ldr, int* piv, double* sh, int* s_int) {
-  if (d > kWarpMaxD) return chol_piv_dd(Gh, Gl, d, thresh, R, ldr, piv, sh);
+  if constexpr (!LEAN) {
+    if (d > kWarpMaxD) return chol_piv_dd(Gh, Gl, d, thresh, R, ldr, piv, sh);
+  }
   if (threadIdx.x < 32) {
     const int k = chol_piv_dd_warp(Gh, Gl, d, thresh, R, ldr, piv);
     if (threadIdx.x == 0) *s_int = k;
@@ -814,11 +965,14 @@ __device__ __forceinline__ int chol_any(double* Gh, double* Gl, int d, double th
   return *s_int;
 }
 
+template <bool LEAN = false>
 __device__ __forceinline__ int svd_r_any(const double* R, int ldr, int k, int m, const int* piv,
                                          const SvdWork& w, double budget2, int cap, double* U,
                                          int ldu, double* margin_out, int* s_int) {
-  if (k > kWarpMaxD)
-    return svd_from_r(R, ldr, k, m, piv, w, budget2, cap, U, ldu, margin_out, s_int);
+  if constexpr (!LEAN) {
+    if (k > kWarpMaxD)
+      return svd_from_r(R, ldr, k, m, piv, w, budget2, cap, U, ldu, margin_out, s_int);
+  }
   if (threadIdx.x < 32) {
     const int t = svd_from_r_warp(R, ldr, k, m, piv, w, budget2, cap, U, ldu, margin_out);
     if (threadIdx.x == 0) *s_int = t;
@@ -1171,7 +1325,13 @@ __host__ __device__ inline GramPlan gram_plan(int n1, int n3, int RM1, int RM2, 
 }
 
 // One output per call (one CTA of NT threads).  SPILL: see gram_plan.
-template <int Q, bool SPILL>
+// LEAN: the launch's summed ranks stay below the mode sizes and its Gram
+// dimensions within the single-warp factorizations (RM1 < n1, RM2 <= n3,
+// D <= kWarpMaxD: the bulk bins of the step), so only the W route, the
+// grouped QR of last^T and the warp-level Cholesky / Jacobi are compiled in
+// -- a third of the instructions of the general body (the general kernel
+// showed 14 % of its warp stalls waiting on instruction fetch).
+template <int Q, bool SPILL, bool LEAN = false>
 __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o, double* sm,
                                                 int* s_meta) {
   const int n1 = p.n1, n2 = p.n2, n3 = p.n3;
@@ -1249,7 +1409,7 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
   materialise_outer(F, lastT, terms, K, n1, n2, n3);
   __syncthreads();
   PROF(0);
-  if (R2 <= NT) {
+  if (LEAN || R2 <= NT) {
     qr_grp(lastT, n3, n3, R2, tau, sh);
   } else {
     qr_inplace(lastT, n3, n3, R2, tau, sh);
@@ -1264,7 +1424,7 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
   //   A_(1) A_(1)^T = C C^T with C = F Pi R_W^T (n1 x k); sigma and U1 from
   //   the column-pivoted QR + Jacobi of C^T (svd_left).  R1 x R1 work per
   //   slice instead of n1 x n1 -- the common case of low-rank sums.
-  const bool wroute = R1 < n1;
+  const bool wroute = LEAN || R1 < n1;
   const int d1 = wroute ? R1 : n1;
   int ei[Q], ej[Q];
   double gh[Q], gl[Q];
@@ -1278,7 +1438,7 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
       else ei[q] = ej[q] = -1;
     }
   }
-  if (wroute) {
+  if (LEAN || wroute) {
     for (int j0 = 0; j0 < n2; j0 += JB) {
       const int jn = min(JB, n2 - j0);
       __syncthreads();
@@ -1318,14 +1478,14 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
       PROF(4);
       gram_rows_acc<Q>(gh, gl, ei, ej, Tb, d1, jn * q3);
     }
-  } else {
+  } else if constexpr (!LEAN) {
     for (int j = 0; j < n2; ++j) {
       __syncthreads();
       stage_slice(Ms, terms, K, n1, n2, j);
       __syncthreads();
-      left_times_blockdiag(XP, n1, F, n1, n1, R2, Ms, terms, colterm);
+      left_times_blockdiag(XP, n1, F, n1, n1, R2, Ms, terms, colterm, p.no_dmma ? 0 : R1);
       __syncthreads();
-      times_r3t(Tb, n1, false, XP, n1, n1, q3, R2, lastT, n3);
+      times_r3t(Tb, n1, false, XP, n1, n1, q3, R2, lastT, n3, !p.no_dmma);
       __syncthreads();
       gram_rows_acc<Q>(gh, gl, ei, ej, Tb, d1, q3);
     }
@@ -1340,7 +1500,7 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
   double norm2 = trace;
   int k1 = 0;
   if (wroute && trace > 0.0 && isfinite(trace)) {
-    k1 = chol_any(G, Gl, d1, 1e-31 * trace, Rc, D, piv, sh, &s_meta[6]);
+    k1 = chol_any<LEAN>(G, Gl, d1, 1e-31 * trace, Rc, D, piv, sh, &s_meta[6]);
     // M = C^T (k1 x n1, ld D1) into Tb: M(r, i) = sum_{v >= r} R_W(r, v) F(i, piv[v])
     double l2 = 0.0;
     for2d(k1, n1, [&](int r, int i) {
@@ -1383,7 +1543,7 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
   const SvdWork sw{p.prof, Xs, vn, sig, sraw, piv, perm, sh, mx};
   double mg1 = 0.0;
   int t1;
-  if (wroute && k1 <= kWarpMaxD) {
+  if (LEAN || (wroute && k1 <= kWarpMaxD)) {
     // sigma and U1 of C (n1 x k1, C^T in Tb) through its k1 x k1 Gram:
     // exact dd Gram -> pivoted dd Cholesky Rg -> Jacobi on Rg^T gives sigma
     // and the right vectors V (into XP, k1 x t1); U1 = C V / sigma.  The
@@ -1403,9 +1563,9 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
     gram_rows_acc<Q>(gh, gl, ei, ej, Tb, D1, n1);
     gram_store<Q>(G, Gl, k1, gh, gl, ei, ej);
     __syncthreads();
-    const int kc = chol_any(G, Gl, k1, cthresh, Rc, D, piv, sh, &s_meta[6]);
+    const int kc = chol_any<LEAN>(G, Gl, k1, cthresh, Rc, D, piv, sh, &s_meta[6]);
     double* V = XP;  // k1 x t1
-    t1 = svd_r_any(Rc, D, kc, k1, piv, sw, budget2, p.cap, V, k1, &mg1, &s_meta[4]);
+    t1 = svd_r_any<LEAN>(Rc, D, kc, k1, piv, sw, budget2, p.cap, V, k1, &mg1, &s_meta[4]);
     for2d(n1, t1, [&](int i, int r) {
       double a0 = 0.0, a1 = 0.0;
       int v = 0;
@@ -1417,13 +1577,15 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
       U1[i + n1 * r] = (a0 + a1) / sig[r];
     });
     __syncthreads();
-  } else if (wroute) {
-    PROF(3);
-    t1 = svd_left(Tb, D1, k1, n1, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
-  } else {
-    k1 = chol_any(G, Gl, n1, cthresh, Rc, D, piv, sh, &s_meta[6]);
-    PROF(3);
-    t1 = svd_r_any(Rc, D, k1, n1, piv, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
+  } else if constexpr (!LEAN) {
+    if (wroute) {
+      PROF(3);
+      t1 = svd_left(Tb, D1, k1, n1, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
+    } else {
+      k1 = chol_any(G, Gl, n1, cthresh, Rc, D, piv, sh, &s_meta[6]);
+      PROF(3);
+      t1 = svd_r_any(Rc, D, k1, n1, piv, sw, budget2, p.cap, U1, n1, &mg1, &s_meta[4]);
+    }
   }
   if (p.margins && threadIdx.x == 0) p.margins[2 * o] = mg1;
   PROF(5);
@@ -1462,10 +1624,11 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
       __syncthreads();
     }
     PROF(11);
-    left_times_blockdiag_b(X2j, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn);
+    left_times_blockdiag_b(X2j, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn,
+                           (LEAN || p.no_dmma) ? 0 : R1);
     __syncthreads();
     // S_j^T (q3 x t1) at column block jj
-    times_r3t_b(Tb, q3, q3 * t1, X2j, t1, t1 * R2, t1, q3, R2, lastT, n3, jn);
+    times_r3t_b(Tb, q3, q3 * t1, X2j, t1, t1 * R2, t1, q3, R2, lastT, n3, jn, !LEAN && !p.no_dmma);
     __syncthreads();
     PROF(8);
     gram_rows_acc<Q>(gh, gl, ei, ej, Tb, q3, jn * t1);
@@ -1474,11 +1637,11 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
   gram_store<Q>(G, Gl, q3, gh, gl, ei, ej);
   __syncthreads();
   PROF(6);
-  const int k2 = chol_any(G, Gl, q3, cthresh, Rc, D, piv, sh, &s_meta[6]);
+  const int k2 = chol_any<LEAN>(G, Gl, q3, cthresh, Rc, D, piv, sh, &s_meta[6]);
   PROF(7);
   double mg2 = 0.0;
   double* W2 = Tb;  // V2 (q3 x t2), ld D3
-  const int t2 = svd_r_any(Rc, D, k2, q3, piv, sw, budget2, p.cap, W2, D3, &mg2, &s_meta[5]);
+  const int t2 = svd_r_any<LEAN>(Rc, D, k2, q3, piv, sw, budget2, p.cap, W2, D3, &mg2, &s_meta[5]);
   PROF(9);
   if (threadIdx.x == 0) {
     if (p.margins) p.margins[2 * o + 1] = mg2;
@@ -1551,10 +1714,25 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
     if (!keepX2) {
       stage_slices(Ms, p.MSMAX, terms, K, n1, n2, j0, jn);
       __syncthreads();
-      left_times_blockdiag_b(X2, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn);
+      left_times_blockdiag_b(X2, t1, t1 * R2, XP, n1, t1, R2, Ms, p.MSMAX, terms, colterm, jn,
+                             (LEAN || p.no_dmma) ? 0 : R1);
       __syncthreads();
     }
     // middle_j = (P blockdiag(M_j)) Z
+    if (!LEAN && !p.no_dmma && dmma_worth(t1, t2, R2)) {
+      double* dm = dmid + (long long)j0 * t1 * t2;
+      dmma_gemm(
+          jn, t1, t2,
+          [&](int q, int i, int k) { return (i < t1 && k < R2) ? X2[q * t1 * R2 + i + t1 * k] : 0.0; },
+          [&](int, int k, int j) { return (k < R2 && j < t2) ? Z[k + RM2 * j] : 0.0; },
+          [&](int q, int i, int j, double v) {
+            if (i < t1 && j < t2) dm[(long long)q * t1 * t2 + i + t1 * j] = v;
+          },
+          [&](int, int& kb, int& ke) {
+            kb = 0;
+            ke = R2;
+          });
+    } else
     for2d(t1, jn * t2, [&](int r, int js) {
       const int jj = js / t2, s = js - jj * t2;
       const double* x = X2 + jj * t1 * R2 + r;
@@ -1582,7 +1760,7 @@ __device__ __forceinline__ void round_gram_body(const RoundArgs& p, const int o,
 #ifndef TTDVM_TINY_MINB
 #define TTDVM_TINY_MINB 8
 #endif
-template <int Q, bool SPILL>
+template <int Q, bool SPILL, bool LEAN = false>
 __global__ void __launch_bounds__(NT, SPILL ? 1 : (Q == 0 ? TTDVM_TINY_MINB * 128 / NT : (Q <= 3 ? 512 / NT : (Q <= 10 ? (NT == 128 ? 3 : 1) : 1))))
     round_gram_kernel(RoundArgs p) {
   constexpr int QB = Q == 0 ? 1 : Q;
@@ -1590,7 +1768,7 @@ __global__ void __launch_bounds__(NT, SPILL ? 1 : (Q == 0 ? TTDVM_TINY_MINB * 12
   __shared__ __align__(8) int s_meta[10];  // [8..9]: the operand cache's mbarrier
   if constexpr (!SPILL) {
     const int o = p.olist ? p.olist[blockIdx.x] : blockIdx.x;
-    if (o < p.nout) round_gram_body<QB, false>(p, o, sm, s_meta);
+    if (o < p.nout) round_gram_body<QB, false, LEAN>(p, o, sm, s_meta);
   } else {
     for (int b = blockIdx.x; b < p.nblk; b += gridDim.x) {
       const int o = p.olist ? p.olist[b] : b;
@@ -1640,8 +1818,21 @@ static cudaError_t launch_gram_q(const RoundArgs& a, int grid, size_t smem, cuda
   const int D = D1 > D3 ? D1 : D3;
   const int ne = D * (D + 1) / 2;
   cudaError_t e = cudaSuccess;
+  // the pruned build for the bulk bins (see round_gram_body); TTDVM_LEAN=0
+  // keeps the general kernel (A/B)
+  static const bool lean_on = [] {
+    const char* e = getenv("TTDVM_LEAN");
+    return !(e && *e == '0');
+  }();
+  const bool lean = !SPILL && lean_on && a.RM1 < a.n1 && a.RM2 <= a.n3 && D <= kWarpMaxD;
 #define LAUNCH_Q(QV)                                                                         \
-  {                                                                                          \
+  if (lean && (QV) >= 1 && (QV) <= 5) {                                                      \
+    constexpr int QL = (QV) >= 1 && (QV) <= 5 ? (QV) : 1;                                    \
+    auto kern = round_gram_kernel<QL, false, true>;                                          \
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+    if (e != cudaSuccess) return e;                                                          \
+    kern<<<grid, NT, smem, st>>>(a);                                                         \
+  } else {                                                                                   \
     auto kern = round_gram_kernel<QV, SPILL>;                                                \
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
     if (e != cudaSuccess) return e;                                                          \

@@ -95,6 +95,7 @@ struct RoundArgs {
   int HMAX;                     // rows of the TSQR block buffer
   int MSMAX;                    // doubles of the staged middle slices
   int JB;                       // slices per barrier phase (exact-Gram kernel)
+  int no_dmma;                  // diagnostics (TTDVM_DMMA=0): slice products on the FMA strips
   int OC;                       // doubles of the shared-memory operand cache (0 = off): every
                                 // distinct operand tensor of an output is fetched whole by one
                                 // cp.async.bulk (TMA) at set-up and read from shared memory after

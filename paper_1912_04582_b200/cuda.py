@@ -37,7 +37,7 @@ EXPORTS = (
     "ttdvm_cuda_face_factors", "ttdvm_cuda_wall_densities", "ttdvm_cuda_setup_info",
     "ttdvm_cuda_round_resident", "ttdvm_cuda_phase_report", "ttdvm_cuda_nccl_unique_id",
     "ttdvm_cuda_comm_init", "ttdvm_cuda_set_comm", "ttdvm_cuda_set_partition",
-    "ttdvm_cuda_halo_stats",
+    "ttdvm_cuda_halo_stats", "ttdvm_cuda_lusgs_step", "ttdvm_cuda_lusgs_levels",
 )
 
 OK, EINVAL, EDOMAIN, ENOMEM, ECUDA, ENCCL = range(6)
@@ -109,6 +109,8 @@ def load_library(path: str = LIB_PATH):
         "ttdvm_cuda_set_comm": (C.c_int, [vp, vp, i32, i32]),
         "ttdvm_cuda_set_partition": (C.c_int, [vp, i32, i32, vp, vp, vp, vp, vp]),
         "ttdvm_cuda_halo_stats": (C.c_int, [vp, vp]),
+        "ttdvm_cuda_lusgs_step": (C.c_int, [vp, dbl, dbl, i32, i32]),
+        "ttdvm_cuda_lusgs_levels": (C.c_int, [vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -237,6 +239,16 @@ class Context:
     def step(self, dt: float, eps: float, cap: int = 0, nsteps: int = 1):
         """explicit_step, nsteps times, state resident."""
         self._check(self.lib.ttdvm_cuda_step(self.h, float(dt), float(eps), int(cap), int(nsteps)))
+
+    def lusgs_step(self, dt: float, eps: float, cap: int = 0, niter: int = 1):
+        """SPEC.md:399 lusgs_step over the resident state (ttdvm_cuda_lusgs_step)."""
+        self._check(self.lib.ttdvm_cuda_lusgs_step(self.h, float(dt), float(eps), int(cap),
+                                                   int(niter)))
+
+    def lusgs_levels(self):
+        a, b = C.c_int32(0), C.c_int32(0)
+        self._check(self.lib.ttdvm_cuda_lusgs_levels(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def set_blocks(self, nblocks: int):
         """Cell blocks of the bounded-memory step (0 = automatic)."""
