@@ -10,6 +10,7 @@
 // The state is double-buffered across steps.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -437,10 +438,16 @@ struct Timer {
   ttdvm_ctx* c;
   int phase;
   explicit Timer(ttdvm_ctx* c_, int p) : c(c_), phase(p) {
+    static const char* const kNames[kNPhase] = {
+        "ttdvm:moments",        "ttdvm:shakhov_build", "ttdvm:round_fs",
+        "ttdvm:round_collision", "ttdvm:round_flux",    "ttdvm:round_residual",
+        "ttdvm:round_update",   "ttdvm:bookkeeping",   "ttdvm:wall_densities"};
     c->cur_phase = p;
+    nvtxRangePushA(kNames[p]);  // NVTX range per step phase (no-op without a tool attached)
     if (c->profiling) CK(cudaEventRecord(c->ev0, c->st));
   }
   ~Timer() {
+    nvtxRangePop();
     if (c->profiling) {
       cudaEventRecord(c->ev1, c->st);
       cudaEventSynchronize(c->ev1);
@@ -1690,6 +1697,10 @@ void free_peers(ttdvm_ctx* c) {
 // is grown for the incoming ghosts here, before those kernels are queued.
 void halo_begin(ttdvm_ctx* c, TensorSet& s) {
   if (!c->comm || c->peers.empty()) return;
+  nvtxRangePushA("ttdvm:halo_begin");
+  struct Pop {
+    ~Pop() { nvtxRangePop(); }
+  } pop_;
   NcclApi& a = nccl();
   const int n = c->n;
   ensure_comm_stream(c);
