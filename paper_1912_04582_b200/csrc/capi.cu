@@ -50,6 +50,11 @@ TTDVM_GRAM_API
 }
 namespace g32 {
 TTDVM_GRAM_API
+// the bulk rank bins as a pipeline of six phase kernels (round_pipe.cuh)
+bool round_pipe_eligible(const RoundArgs& p);
+long long round_pipe_record_doubles(const RoundArgs& p);
+cudaError_t launch_round_pipe(const RoundArgs& p, int first, int count, double* rec,
+                              cudaStream_t st);
 }
 #undef TTDVM_GRAM_API
 using g128::round_gram_smem_bytes;  // the plan does not depend on the CTA width
@@ -373,6 +378,7 @@ struct ttdvm_ctx {
   DevBuf<double> d_margins;
   DevBuf<int> d_bins, d_olist;  // rank bins of the current rounding launch
   DevBuf<double> d_gscratch;     // per-CTA slices of spill-plan rounding launches
+  DevBuf<double> d_pipe;         // per-output records of the phase-pipeline launches
   DevBuf<long long> d_tmp_off;
   DevBuf<double> d_tmp;
   bool profiling = false;
@@ -618,6 +624,9 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     int bin, count, rm1, rm2, ms, jb;
     bool spill, wide, narrow;
     int oc = 0;  // doubles of the operand cache (TMA bulk copies of whole operands), 0 = off
+    bool pipe = false;        // six phase kernels, one warp per output (round_pipe.cuh)
+    size_t pipe_off = 0;      // this launch's records in d_pipe (doubles)
+    long long pipe_stride = 0;
   };
   // 256-thread CTAs from Gram dimension TTDVM_WIDE_D (default 16) up: the
   // measured crossover between the short-phase small tiles (128 threads, four
@@ -714,6 +723,28 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
                                  8 * (size_t)((l.oc + 1) & ~1) > kSmemMax)
         --l.jb;
     }
+    // Bulk bins (the LEAN condition) take the phase pipeline: TTDVM_PIPE=0
+    // keeps the one-kernel path (A/B), TTDVM_PIPE_MIN = fewest outputs worth
+    // six launches per chunk.
+    static const int pipe_mode = [] {
+      const char* e = getenv("TTDVM_PIPE");
+      return e ? atoi(e) : 1;
+    }();
+    static const int pipe_min = [] {
+      const char* e = getenv("TTDVM_PIPE_MIN");
+      return e ? atoi(e) : 2048;
+    }();
+    if (pipe_mode > 0 && !use_tsqr && !l.spill && l.count >= pipe_min) {
+      RoundArgs ra = a;
+      ra.RM1 = l.rm1;
+      ra.RM2 = l.rm2;
+      ra.MSMAX = l.ms;
+      if (g32::round_pipe_eligible(ra)) {
+        l.pipe = true;
+        l.pipe_stride = g32::round_pipe_record_doubles(ra);
+        l.oc = 0;
+      }
+    }
     if (l.spill && round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, true) > kSmemMax)
       throw Fail{TTDVM_ENOMEM, "rounding working set exceeds shared memory (n=" +
                                    std::to_string(n) + ", summed ranks " +
@@ -809,6 +840,16 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
         scratch_need = std::max(scratch_need, g * (size_t)round_gram_spill_doubles(n, n, l.rm1, l.rm2));
       }
       if (scratch_need) c->d_gscratch.alloc(scratch_need);
+      // records of the pipelined bins: one region per bin (bins run
+      // concurrently), each a chunk of at most kPipeChunk outputs
+      constexpr int kPipeChunk = 65536;
+      size_t pipe_need = 0;
+      for (Launch& l : plan) {
+        if (!l.pipe) continue;
+        l.pipe_off = pipe_need;
+        pipe_need += (size_t)std::min(l.count, kPipeChunk) * (size_t)l.pipe_stride;
+      }
+      if (pipe_need) c->d_pipe.alloc(pipe_need);
       bool used_aux[3] = {false, false, false};
       if (fork) {
         if (!c->fork_ev) {
@@ -859,10 +900,18 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
           CK(cudaEventCreate(&d1));
           CK(cudaEventRecord(d0, c->st));
         }
-        CK(l.wide     ? g256::launch_round_gram(a, grid, lst)
-           : l.narrow ? g32::launch_round_gram(a, grid, lst)
-                      : g128::launch_round_gram(a, grid, lst));
-        c->launches += 1;
+        if (l.pipe) {
+          for (int f0 = 0; f0 < l.count; f0 += kPipeChunk) {
+            const int cnt = std::min(kPipeChunk, l.count - f0);
+            CK(g32::launch_round_pipe(a, f0, cnt, c->d_pipe.p + l.pipe_off, lst));
+            c->launches += 6;
+          }
+        } else {
+          CK(l.wide     ? g256::launch_round_gram(a, grid, lst)
+             : l.narrow ? g32::launch_round_gram(a, grid, lst)
+                        : g128::launch_round_gram(a, grid, lst));
+          c->launches += 1;
+        }
         if (dlog) {  // diagnostics only: per-bin device time (serialises the launches)
           CK(cudaEventRecord(d1, c->st));
           CK(cudaEventSynchronize(d1));
@@ -874,7 +923,8 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
                   "[ttdvm bin] phase %d bin %d outputs %d summed ranks %dx%d D %d jb %d oc %d %s%s grid %d:"
                   " %.2f ms\n",
                   c->cur_phase, l.bin, l.count, l.rm1, l.rm2, gram_d(l.rm1, l.rm2), l.jb, l.oc,
-                  l.wide ? "g256" : (l.narrow ? "g32" : "g128"), l.spill ? " spill" : "", grid, ms);
+                  l.pipe ? "pipe" : (l.wide ? "g256" : (l.narrow ? "g32" : "g128")),
+                  l.spill ? " spill" : "", grid, ms);
         }
       }
       for (int k = 0; k < 3; ++k)
@@ -2177,6 +2227,7 @@ int ttdvm_cuda_destroy(ttdvm_ctx* c) {
   for (auto* v : {&c->bt_flux, &c->bt_res, &c->bt_upd})
     for (TermList& t : *v) t.free();
   c->d_gscratch.free();
+  c->d_pipe.free();
   c->d_nodes.free();
   c->d_weights.free();
   c->d_factors.free();

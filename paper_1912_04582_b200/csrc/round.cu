@@ -30,6 +30,8 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "linalg.cuh"
 
 namespace ttdvm {
@@ -1891,6 +1893,8 @@ cudaError_t launch_round_gram(const RoundArgs& a, int nblocks, cudaStream_t st) 
                       8 * (size_t)((a.OC + 1) & ~1);
   return launch_gram_q<false>(a, nblocks, smem, st, nullptr);
 }
+
+#include "round_pipe.cuh"
 
 }  // namespace RG_NS
 
