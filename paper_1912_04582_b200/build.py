@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libttdvm_cuda.so")
-SOURCES = ["round.cu", "round256.cu", "round32.cu", "physics.cu", "facefactor.cu", "capi.cu"]
+SOURCES = ["round.cu", "round256.cu", "round512.cu", "round32.cu", "physics.cu", "facefactor.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr"]
@@ -33,7 +33,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(CSRC, s.replace(".cu", ".o"))
         objs.append(o)
         deps = [os.path.join(CSRC, s), *headers]
-        if s in ("round256.cu", "round32.cu"):  # include round.cu
+        if s in ("round256.cu", "round512.cu", "round32.cu"):  # include round.cu
             deps.append(os.path.join(CSRC, "round.cu"))
         if not force and os.path.exists(o) and all(
                 os.path.getmtime(d) <= os.path.getmtime(o) for d in deps if os.path.exists(d)):

@@ -48,6 +48,9 @@ TTDVM_GRAM_API
 namespace g256 {
 TTDVM_GRAM_API
 }
+namespace g512 {
+TTDVM_GRAM_API
+}
 namespace g32 {
 TTDVM_GRAM_API
 // the bulk rank bins as a pipeline of six phase kernels (round_pipe.cuh)
@@ -624,6 +627,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     int bin, count, rm1, rm2, ms, jb;
     bool spill, wide, narrow;
     int oc = 0;  // doubles of the operand cache (TMA bulk copies of whole operands), 0 = off
+    bool xwide = false;       // 512-thread CTAs (round512.cu): high-rank, one-CTA-per-SM bins
     bool pipe = false;        // six phase kernels, one warp per output (round_pipe.cuh)
     size_t pipe_off = 0;      // this launch's records in d_pipe (doubles)
     long long pipe_stride = 0;
@@ -693,6 +697,15 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     Launch l{b, bcount[b], std::max(1, bm[0]), std::max(1, bm[1]), std::max(1, bm[2]), 1, false,
              false, false};
     l.wide = gram_d(l.rm1, l.rm2) >= wide_d;
+    // 512-thread CTAs from Gram dimension TTDVM_XWIDE_D up (default 32: the
+    // bins whose plan leaves one CTA per SM); 0 = never.  Measured same-box:
+    // config 3 (D = 32) 101k -> 112k tensors/s, config-4 flux phase -7 %,
+    // config-5 residuals -9 %; from D = 24 it is 25 % slower on config 4.
+    static const int xwide_d = [] {
+      const char* e = getenv("TTDVM_XWIDE_D");
+      return e ? atoi(e) : 32;
+    }();
+    l.xwide = xwide_d > 0 && gram_d(l.rm1, l.rm2) >= xwide_d;
     l.narrow = !l.wide && gram_d(l.rm1, l.rm2) <= narrow_d;
     // working sets above the shared-memory budget (n = 64, summed ranks of
     // ~100 and more) take the spill plan: F, last^T, XP and the Gram region
@@ -833,8 +846,9 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
         ra.RM2 = l.rm2;
         ra.MSMAX = l.ms;
         ra.JB = l.jb;
-        CK(l.wide ? g256::round_gram_resident(ra, &resident)
-                  : g128::round_gram_resident(ra, &resident));
+        CK(l.xwide  ? g512::round_gram_resident(ra, &resident)
+           : l.wide ? g256::round_gram_resident(ra, &resident)
+                    : g128::round_gram_resident(ra, &resident));
         if (resident <= 0) throw Fail{TTDVM_ENOMEM, "spill rounding plan does not fit an SM"};
         const size_t g = (size_t)std::min(l.count, resident);
         scratch_need = std::max(scratch_need, g * (size_t)round_gram_spill_doubles(n, n, l.rm1, l.rm2));
@@ -885,8 +899,9 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
         int grid = l.count;
         if (l.spill) {
           int resident = 0;
-          CK(l.wide ? g256::round_gram_resident(a, &resident)
-                    : g128::round_gram_resident(a, &resident));
+          CK(l.xwide  ? g512::round_gram_resident(a, &resident)
+             : l.wide ? g256::round_gram_resident(a, &resident)
+                      : g128::round_gram_resident(a, &resident));
           if (resident <= 0) throw Fail{TTDVM_ENOMEM, "spill rounding plan does not fit an SM"};
           grid = std::min(l.count, resident);
           a.gstride = round_gram_spill_doubles(n, n, l.rm1, l.rm2);
@@ -907,7 +922,8 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
             c->launches += 6;
           }
         } else {
-          CK(l.wide     ? g256::launch_round_gram(a, grid, lst)
+          CK(l.xwide    ? g512::launch_round_gram(a, grid, lst)
+             : l.wide   ? g256::launch_round_gram(a, grid, lst)
              : l.narrow ? g32::launch_round_gram(a, grid, lst)
                         : g128::launch_round_gram(a, grid, lst));
           c->launches += 1;
@@ -923,7 +939,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
                   "[ttdvm bin] phase %d bin %d outputs %d summed ranks %dx%d D %d jb %d oc %d %s%s grid %d:"
                   " %.2f ms\n",
                   c->cur_phase, l.bin, l.count, l.rm1, l.rm2, gram_d(l.rm1, l.rm2), l.jb, l.oc,
-                  l.pipe ? "pipe" : (l.wide ? "g256" : (l.narrow ? "g32" : "g128")),
+                  l.pipe ? "pipe" : (l.xwide ? "g512" : (l.wide ? "g256" : (l.narrow ? "g32" : "g128"))),
                   l.spill ? " spill" : "", grid, ms);
         }
       }

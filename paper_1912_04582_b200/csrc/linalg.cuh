@@ -16,7 +16,8 @@ namespace {
 #ifndef TTDVM_ROUND_NT
 #define TTDVM_ROUND_NT 128
 #endif
-static_assert(TTDVM_ROUND_NT == kRoundThreads || TTDVM_ROUND_NT == 256 || TTDVM_ROUND_NT == 32,
+static_assert(TTDVM_ROUND_NT == kRoundThreads || TTDVM_ROUND_NT == 256 || TTDVM_ROUND_NT == 32 ||
+                  TTDVM_ROUND_NT == 512,
               "CTA width");
 constexpr int NT = TTDVM_ROUND_NT;
 constexpr int NW = NT / 32;
@@ -98,7 +99,7 @@ __device__ __forceinline__ void larfg(double alpha, double sigma2, double& beta,
 // lambda (instruction-cache footprint matters: the rounding kernel is
 // latency-bound and several CTAs per SM run different phases).  No
 // barriers or shuffles may be used inside f.
-constexpr int LOG_NT = NT == 32 ? 5 : (NT == 64 ? 6 : (NT == 128 ? 7 : 8));
+constexpr int LOG_NT = NT == 32 ? 5 : (NT == 64 ? 6 : (NT == 128 ? 7 : (NT == 256 ? 8 : 9)));
 template <class Fn>
 __device__ __forceinline__ void for2d(int rows, int cols, Fn&& f) {
   if (rows <= 0 || cols <= 0) return;

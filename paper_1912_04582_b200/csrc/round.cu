@@ -1299,7 +1299,9 @@ __global__ void __launch_bounds__(NT, SMALL ? 5 : 3) round_sums_kernel(RoundArgs
 // config-4 face fluxes run best on 128 threads (their phases are short and
 // four CTAs share an SM), the larger ones (cell residuals, config 3,
 // n = 64) on 256 (more threads per dense slice product).
-#if TTDVM_ROUND_NT == 256
+#if TTDVM_ROUND_NT == 512
+#define RG_NS g512
+#elif TTDVM_ROUND_NT == 256
 #define RG_NS g256
 #elif TTDVM_ROUND_NT == 32
 #define RG_NS g32

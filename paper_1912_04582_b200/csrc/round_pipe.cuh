@@ -33,14 +33,16 @@ struct PipeArgs {
   int first;           // first entry of p.olist (or first output) of this chunk
   int count;
   int JB;              // slices per stage in P2 / P4 / P6
-  int oF, oLT, oTau, oG, oU1, oP, oZ, oS;  // record offsets (doubles)
+  int il;              // Gram accumulation with the lane's entries interleaved (pipe_gram_acc)
+  int oF, oLT, oTau, oG, oU1, oP, oZ, oS, oX2;  // record offsets (doubles)
+  int tkeep;           // outputs with t1 <= tkeep keep X2_j = P M_j (all slices) for P6
 };
 
 // record scalars at oS: doubles [0] budget2, [1] cthresh, [2] input doubles
 // (work counter); ints at +4: [0] t1, [1] t2, [2] flag (0 live, 1 finished
 // early or dropped), [3] R1, [4] R2; long long at +8: output offset.
 struct PipeRec {
-  double *F, *LT, *tau, *G, *U1, *P, *Z, *sc;
+  double *F, *LT, *tau, *G, *U1, *P, *Z, *sc, *X2;
   int* iv;
   long long* off;
 };
@@ -55,6 +57,7 @@ __device__ __forceinline__ PipeRec pipe_rec(const PipeArgs& a, int slot) {
   q.P = r + a.oP;
   q.Z = r + a.oZ;
   q.sc = r + a.oS;
+  q.X2 = r + a.oX2;
   q.iv = reinterpret_cast<int*>(r + a.oS + 4);
   q.off = reinterpret_cast<long long*>(r + a.oS + 8);
   return q;
@@ -162,6 +165,32 @@ __device__ __forceinline__ void pipe_zj(double* Tb, const double* Ms, int msmax,
   }
 }
 
+// gram_rows_acc with the Q entries of a lane advanced together: one column
+// loop for all of them (a third of the loop overhead at Q = 3) and Q
+// independent double-double chains in flight.  Every entry still sums its
+// columns in ascending order, so the Gram is bitwise that of gram_rows_acc.
+template <int Q>
+__device__ __forceinline__ void pipe_gram_acc(double (&gh)[Q], double (&gl)[Q], const int (&ei)[Q],
+                                              const int (&ej)[Q], const double* T, int ldt,
+                                              int ncol) {
+  const double* pa[Q];
+  const double* pb[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    pa[q] = T + (ei[q] < 0 ? 0 : ei[q]);
+    pb[q] = T + (ei[q] < 0 ? 0 : ej[q]);
+  }
+#pragma unroll 2
+  for (int c = 0; c < ncol; ++c) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (ei[q] >= 0) dd_fma_acc(gh[q], gl[q], *pa[q], *pb[q]);
+      pa[q] += ldt;
+      pb[q] += ldt;
+    }
+  }
+}
+
 template <int Q>
 __device__ __forceinline__ void pipe_gram_init(int d, int (&ei)[Q], int (&ej)[Q], double (&gh)[Q],
                                                double (&gl)[Q]) {
@@ -205,7 +234,8 @@ __global__ void __launch_bounds__(NT, 24) pipe_gram1_kernel(PipeArgs a) {
     __syncthreads();
     pipe_zj(Tb, Ms, p.MSMAX, pt.terms, pt.rowterm, R3, D3, R1, q3, jn);
     __syncthreads();
-    gram_rows_acc<Q>(gh, gl, ei, ej, Tb, R1, jn * q3);
+    if (a.il) pipe_gram_acc<Q>(gh, gl, ei, ej, Tb, R1, jn * q3);
+    else gram_rows_acc<Q>(gh, gl, ei, ej, Tb, R1, jn * q3);
   }
   gram_store<Q>(r.G, r.G + RM1 * RM1, R1, gh, gl, ei, ej);
 }
@@ -361,9 +391,14 @@ __global__ void __launch_bounds__(NT, 24) pipe_gram2_kernel(PipeArgs a) {
     __syncthreads();
     left_times_blockdiag_b(X2, t1, t1 * R2, XP, D1, t1, R2, Ms, p.MSMAX, pt.terms, pt.colterm, jn);
     __syncthreads();
+    if (t1 <= a.tkeep) {  // low-rank outputs keep P M_j for the output stage (no restaging in P6)
+      double* xg = r.X2 + (long long)j0 * t1 * R2;
+      for (int e = threadIdx.x; e < jn * t1 * R2; e += NT) xg[e] = X2[e];
+    }
     times_r3t_b(Tb, q3, q3 * t1, X2, t1, t1 * R2, t1, q3, R2, R3, D3, jn);
     __syncthreads();
-    gram_rows_acc<Q>(gh, gl, ei, ej, Tb, q3, jn * t1);
+    if (a.il) pipe_gram_acc<Q>(gh, gl, ei, ej, Tb, q3, jn * t1);
+    else gram_rows_acc<Q>(gh, gl, ei, ej, Tb, q3, jn * t1);
   }
   gram_store<Q>(r.G, r.G + RM2 * RM2, q3, gh, gl, ei, ej);
 }
@@ -485,11 +520,31 @@ __global__ void __launch_bounds__(NT, 24) pipe_middle_kernel(PipeArgs a) {
   double* X2 = Z + RM2 * RM2;             // JB x t1 x R2
   double* Ms = X2 + JB * D1 * RM2;        // JB x MSMAX
   PipeTerms pt = pipe_terms(Ms + JB * p.MSMAX, RM1, RM2);
+  double* dmid = p.out.base + r.off[0] + (long long)n1 * t1;
+  for (int e = threadIdx.x; e < RM2 * t2; e += NT) Z[e] = r.Z[e];
+  if (t1 <= a.tkeep) {
+    // X2_j = P M_j of every slice was kept by P4: one product, no staging
+    const int R2k = r.iv[4];
+    const double* xg = r.X2;
+    __syncthreads();
+    for2d(t1, n2 * t2, [&](int rr, int js) {
+      const int jj = js / t2, s = js - jj * t2;
+      const double* x = xg + (long long)jj * t1 * R2k + rr;
+      const double* z = Z + RM2 * s;
+      double a0 = 0.0, a1 = 0.0;
+      int b = 0;
+      for (; b + 1 < R2k; b += 2) {
+        a0 += x[t1 * b] * z[b];
+        a1 += x[t1 * (b + 1)] * z[b + 1];
+      }
+      if (b < R2k) a0 += x[t1 * b] * z[b];
+      dmid[(long long)jj * t1 * t2 + rr + t1 * s] = a0 + a1;
+    });
+    return;
+  }
   int K, R1, R2;
   setup_terms(p, o, pt.terms, pt.rowterm, pt.colterm, s_meta, K, R1, R2);
   for (int e = threadIdx.x; e < D1 * R1; e += NT) XP[e] = r.P[e];
-  for (int e = threadIdx.x; e < RM2 * t2; e += NT) Z[e] = r.Z[e];
-  double* dmid = p.out.base + r.off[0] + (long long)n1 * t1;
   for (int j0 = 0; j0 < n2; j0 += JB) {
     const int jn = min(JB, n2 - j0);
     __syncthreads();
@@ -536,6 +591,13 @@ static void pipe_layout(PipeArgs& a) {
   o += even((long long)RM2 * RM2);
   a.oS = (int)o;
   o += 12;
+  a.oX2 = (int)o;
+  static const int tkeep_env = [] {  // TTDVM_PIPE_TKEEP=0: always restage in P6 (A/B)
+    const char* e = getenv("TTDVM_PIPE_TKEEP");
+    return e ? atoi(e) : 2;
+  }();
+  a.tkeep = std::min(tkeep_env, RM1);
+  o += even((long long)p.n2 * a.tkeep * RM2);
   a.stride = (o + 15) / 16 * 16;
 }
 
@@ -563,7 +625,19 @@ cudaError_t launch_round_pipe(const RoundArgs& p, int first, int count, double* 
   a.count = count;
   pipe_layout(a);
   const int n1 = p.n1, n3 = p.n3, RM1 = p.RM1, RM2 = p.RM2, D = RM1 > RM2 ? RM1 : RM2;
-  a.JB = std::max(1, std::min(p.n2, 512 / std::max(1, RM1 * RM2)));
+  // slices per stage: about 512 doubles of Z_j per batch (TTDVM_PIPE_JB overrides, A/B)
+  static const int jb_env = [] {
+    const char* e = getenv("TTDVM_PIPE_JB");
+    return e ? atoi(e) : 0;
+  }();
+  a.JB = std::max(1, std::min(p.n2, jb_env > 0 ? jb_env : 512 / std::max(1, RM1 * RM2)));
+  // TTDVM_PIPE_IL=1: the lane's Gram entries interleaved in one column loop
+  // (measured neutral at Q = 3, 6 % slower at Q = 5: off by default)
+  static const int il_env = [] {
+    const char* e = getenv("TTDVM_PIPE_IL");
+    return e ? atoi(e) : 0;
+  }();
+  a.il = il_env;
   const size_t tb = pipe_terms_bytes(RM1, RM2);
   const size_t small = (size_t)(5 * D * D + 3 * D + 32) * 8 + (size_t)2 * D * 4 + 16;
   const size_t s1 = (size_t)(n1 * RM1 + n3 * RM2 + n3 + 32) * 8 + tb;
