@@ -34,6 +34,7 @@ struct PipeArgs {
   int count;
   int JB;              // slices per stage in P2 / P4 / P6
   int il;              // Gram accumulation with the lane's entries interleaved (pipe_gram_acc)
+  int zt;              // P2: Z_j rows per lane, transposed Z buffer, vector loads in the Gram loop
   int oF, oLT, oTau, oG, oU1, oP, oZ, oS, oX2;  // record offsets (doubles)
   int tkeep;           // outputs with t1 <= tkeep keep X2_j = P M_j (all slices) for P6
 };
@@ -84,6 +85,11 @@ __device__ __forceinline__ PipeTerms pipe_terms(double* at, int RM1, int RM2) {
 static size_t pipe_terms_bytes(int RM1, int RM2) {
   return (((size_t)(RM1 + RM2 + 1) * 4 + 7) / 8) * 8 + sizeof(TermInfo) * kMaxTerms;
 }
+
+// leading dimension of P2's transposed Z buffer: the batch's columns rounded
+// up to even (16-byte rows) plus two, so consecutive rows start 16 bytes
+// apart modulo the bank period
+__host__ __device__ inline int pipe_ldz(int JB, int D3) { return ((JB * D3 + 1) & ~1) + 2; }
 
 // R3 (upper trapezoid of the factored last^T, rows < q3) from the record
 // into shared memory with leading dimension ld
@@ -204,6 +210,76 @@ __device__ __forceinline__ void pipe_gram_init(int d, int (&ei)[Q], int (&ej)[Q]
   }
 }
 
+// Z_j of the W route with ONE (row a, slice jj) PAIR PER LANE: the lane keeps
+// its row of M_t in registers and walks the q3 columns, so a multiply-add
+// costs one shared-memory load of R3 (broadcast among the lanes of a summand)
+// instead of two loads plus the per-element index arithmetic of pipe_zj.
+// Stored transposed, Zt(a, jj * q3 + c) at Zt[jj * q3 + c + ldz * a]: the
+// Gram loop then reads consecutive columns with 16-byte loads.  R3 is zero
+// below its diagonal and padded by four zero columns, so the b loop needs no
+// bounds; every sum still adds its terms in ascending b (the skipped ones
+// are exact zeros): the values are those of pipe_zj.
+__device__ __forceinline__ void pipe_zj_rows(double* Zt, int ldz, const double* Ms, int msmax,
+                                             const TermInfo* terms, const int* rowterm,
+                                             const double* R3, int ldr, int R1, int q3, int jn) {
+  for (int pr = threadIdx.x; pr < R1 * jn; pr += NT) {
+    const int jj = pr / R1, a2 = pr - jj * R1;
+    const TermInfo& t = terms[rowterm[a2]];
+    const int r1 = t.r1, r2 = t.r2;
+    const double* mj = Ms + jj * msmax + t.ms + (a2 - t.off1);
+    const double* lb = R3 + ldr * t.off2;
+    double* z = Zt + jj * q3 + ldz * a2;
+    if (r2 <= 4) {
+      const double m0 = mj[0], m1 = r2 > 1 ? mj[r1] : 0.0, m2 = r2 > 2 ? mj[2 * r1] : 0.0,
+                   m3 = r2 > 3 ? mj[3 * r1] : 0.0;
+#pragma unroll 4
+      for (int c = 0; c < q3; ++c) {
+        double sacc = m0 * lb[c];
+        sacc = fma(m1, lb[c + ldr], sacc);
+        sacc = fma(m2, lb[c + 2 * ldr], sacc);
+        sacc = fma(m3, lb[c + 3 * ldr], sacc);
+        z[c] = sacc;
+      }
+    } else {
+      for (int c = 0; c < q3; ++c) {
+        double sacc = 0.0;
+        for (int b = max(0, c - t.off2); b < r2; ++b) sacc += lb[c + ldr * b] * mj[r1 * b];
+        z[c] = sacc;
+      }
+    }
+  }
+}
+
+// Gram accumulation over the rows of the transposed buffer (entry (i, j) =
+// sum_c Zt[c + ld i] Zt[c + ld j]), columns in ascending order, four per
+// iteration through 16-byte loads.
+template <int Q>
+__device__ __forceinline__ void pipe_gram_acc_t(double (&gh)[Q], double (&gl)[Q],
+                                                const int (&ei)[Q], const int (&ej)[Q],
+                                                const double* T, int ld, int ncol) {
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    if (ei[q] < 0) continue;
+    const double* x = T + ld * ei[q];
+    const double* y = T + ld * ej[q];
+    double h = gh[q], l = gl[q];
+    int c = 0;
+    for (; c + 4 <= ncol; c += 4) {
+      const double2 x0 = *reinterpret_cast<const double2*>(x + c);
+      const double2 x1 = *reinterpret_cast<const double2*>(x + c + 2);
+      const double2 y0 = *reinterpret_cast<const double2*>(y + c);
+      const double2 y1 = *reinterpret_cast<const double2*>(y + c + 2);
+      dd_fma_acc(h, l, x0.x, y0.x);
+      dd_fma_acc(h, l, x0.y, y0.y);
+      dd_fma_acc(h, l, x1.x, y1.x);
+      dd_fma_acc(h, l, x1.y, y1.y);
+    }
+    for (; c < ncol; ++c) dd_fma_acc(h, l, x[c], y[c]);
+    gh[q] = h;
+    gl[q] = l;
+  }
+}
+
 // ---- P2 ---------------------------------------------------------------------
 template <int Q>
 __global__ void __launch_bounds__(NT, 24) pipe_gram1_kernel(PipeArgs a) {
@@ -215,14 +291,18 @@ __global__ void __launch_bounds__(NT, 24) pipe_gram1_kernel(PipeArgs a) {
   const int o = pipe_output(a, slot);
   const int n1 = p.n1, n2 = p.n2, n3 = p.n3, RM1 = p.RM1, RM2 = p.RM2, JB = a.JB;
   const int D3 = RM2;
-  double* R3 = sm;                        // D3 x RM2
-  double* Tb = R3 + D3 * RM2;             // JB x RM1 x D3
-  double* Ms = Tb + JB * RM1 * D3;        // JB x MSMAX
+  const int ldz = pipe_ldz(JB, D3);
+  double* R3 = sm;                        // D3 x (RM2 + 4), zero below the diagonal and in the pad
+  double* Tb = R3 + ((D3 * (RM2 + 4) + 1) & ~1);  // Z batch (16-byte aligned): JB x RM1 x D3, or
+                                                  // RM1 rows of ldz (transposed)
+  double* Ms = Tb + RM1 * ldz;            // JB x MSMAX
   PipeTerms pt = pipe_terms(Ms + JB * p.MSMAX, RM1, RM2);
   PipeRec r = pipe_rec(a, slot);
   int K, R1, R2;
   setup_terms(p, o, pt.terms, pt.rowterm, pt.colterm, s_meta, K, R1, R2);
   const int q3 = min(n3, R2);
+  for (int e = threadIdx.x; e < D3 * (RM2 + 4); e += NT) R3[e] = 0.0;
+  __syncthreads();
   pipe_load_r3(R3, D3, r.LT, n3, q3, R2);
   int ei[Q], ej[Q];
   double gh[Q], gl[Q];
@@ -232,10 +312,16 @@ __global__ void __launch_bounds__(NT, 24) pipe_gram1_kernel(PipeArgs a) {
     __syncthreads();
     stage_slices(Ms, p.MSMAX, pt.terms, K, n1, n2, j0, jn);
     __syncthreads();
-    pipe_zj(Tb, Ms, p.MSMAX, pt.terms, pt.rowterm, R3, D3, R1, q3, jn);
-    __syncthreads();
-    if (a.il) pipe_gram_acc<Q>(gh, gl, ei, ej, Tb, R1, jn * q3);
-    else gram_rows_acc<Q>(gh, gl, ei, ej, Tb, R1, jn * q3);
+    if (a.zt) {
+      pipe_zj_rows(Tb, ldz, Ms, p.MSMAX, pt.terms, pt.rowterm, R3, D3, R1, q3, jn);
+      __syncthreads();
+      pipe_gram_acc_t<Q>(gh, gl, ei, ej, Tb, ldz, jn * q3);
+    } else {
+      pipe_zj(Tb, Ms, p.MSMAX, pt.terms, pt.rowterm, R3, D3, R1, q3, jn);
+      __syncthreads();
+      if (a.il) pipe_gram_acc<Q>(gh, gl, ei, ej, Tb, R1, jn * q3);
+      else gram_rows_acc<Q>(gh, gl, ei, ej, Tb, R1, jn * q3);
+    }
   }
   gram_store<Q>(r.G, r.G + RM1 * RM1, R1, gh, gl, ei, ej);
 }
@@ -638,10 +724,16 @@ cudaError_t launch_round_pipe(const RoundArgs& p, int first, int count, double* 
     return e ? atoi(e) : 0;
   }();
   a.il = il_env;
+  static const int zt_env = [] {  // TTDVM_PIPE_ZT=0: P2 with pipe_zj + gram_rows_acc (A/B)
+    const char* e = getenv("TTDVM_PIPE_ZT");
+    return e ? atoi(e) : 1;
+  }();
+  a.zt = zt_env;
   const size_t tb = pipe_terms_bytes(RM1, RM2);
   const size_t small = (size_t)(5 * D * D + 3 * D + 32) * 8 + (size_t)2 * D * 4 + 16;
   const size_t s1 = (size_t)(n1 * RM1 + n3 * RM2 + n3 + 32) * 8 + tb;
-  const size_t s2 = (size_t)(RM2 * RM2 + a.JB * RM1 * RM2 + a.JB * p.MSMAX) * 8 + tb;
+  const size_t s2 =
+      (size_t)(((RM2 * (RM2 + 4) + 1) & ~1) + RM1 * pipe_ldz(a.JB, RM2) + a.JB * p.MSMAX) * 8 + tb;
   const size_t s3 = (size_t)(2 * n1 * RM1) * 8 + small;
   const size_t s4 = (size_t)(RM2 * RM2 + RM1 * RM1 + 2 * a.JB * RM1 * RM2 + a.JB * p.MSMAX) * 8 + tb;
   const size_t s5 = (size_t)(2 * n3 * RM2 + n3) * 8 + small;
