@@ -631,6 +631,7 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     bool pipe = false;        // six phase kernels, one warp per output (round_pipe.cuh)
     size_t pipe_off = 0;      // this launch's records in d_pipe (doubles)
     long long pipe_stride = 0;
+    int pipe_chunk = 0;       // outputs per pass through the six kernels
   };
   // 256-thread CTAs from Gram dimension TTDVM_WIDE_D (default 16) up: the
   // measured crossover between the short-phase small tiles (128 threads, four
@@ -856,12 +857,14 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
       if (scratch_need) c->d_gscratch.alloc(scratch_need);
       // records of the pipelined bins: one region per bin (bins run
       // concurrently), each a chunk of at most kPipeChunk outputs
-      constexpr int kPipeChunk = 65536;
+      // (at most 65,536 outputs and about 2 GB of records)
       size_t pipe_need = 0;
       for (Launch& l : plan) {
         if (!l.pipe) continue;
+        const long long fit = (2LL << 30) / (8 * std::max<long long>(1, l.pipe_stride));
+        l.pipe_chunk = (int)std::min<long long>(std::min(l.count, 65536), std::max<long long>(8192, fit));
         l.pipe_off = pipe_need;
-        pipe_need += (size_t)std::min(l.count, kPipeChunk) * (size_t)l.pipe_stride;
+        pipe_need += (size_t)l.pipe_chunk * (size_t)l.pipe_stride;
       }
       if (pipe_need) c->d_pipe.alloc(pipe_need);
       bool used_aux[3] = {false, false, false};
@@ -916,8 +919,8 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
           CK(cudaEventRecord(d0, c->st));
         }
         if (l.pipe) {
-          for (int f0 = 0; f0 < l.count; f0 += kPipeChunk) {
-            const int cnt = std::min(kPipeChunk, l.count - f0);
+          for (int f0 = 0; f0 < l.count; f0 += l.pipe_chunk) {
+            const int cnt = std::min(l.pipe_chunk, l.count - f0);
             CK(g32::launch_round_pipe(a, f0, cnt, c->d_pipe.p + l.pipe_off, lst));
             c->launches += 6;
           }

@@ -116,7 +116,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 __device__ void setup_terms(const RoundArgs& p, int o, TermInfo* terms, int* rowterm,
                             int* colterm, int* s_meta, int& K, int& R1, int& R2,
                             double* ocbuf = nullptr, int OC = 0,
-                            unsigned long long* ocbar = nullptr) {
+                            unsigned long long* ocbar = nullptr, bool prefetch = true) {
   const long long t0 = p.term_off ? p.term_off[o] : (long long)o;
   K = p.term_off ? (int)(p.term_off[o + 1] - t0) : 1;
   const int n1 = p.n1, n2 = p.n2, n3 = p.n3;
@@ -209,7 +209,7 @@ __device__ void setup_terms(const RoundArgs& p, int o, TermInfo* terms, int* row
   // later, and their loads sit on the critical path of each phase.
   const double* oc_lo = ocbuf;
   const double* oc_hi = ocbuf + OC;
-  for (int k = 0; k < K; ++k) {
+  for (int k = 0; prefetch && k < K; ++k) {
     const TermInfo& t = terms[k];
     const long long nb = (long long)n1 * t.b1 + (long long)n2 * t.b1 * t.b2 + (long long)t.b2 * n3;
     if (!(OC > 0 && t.base >= oc_lo && t.base < oc_hi)) prefetch_l1(t.base, nb);

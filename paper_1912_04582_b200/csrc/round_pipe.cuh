@@ -35,7 +35,8 @@ struct PipeArgs {
   int JB;              // slices per stage in P2 / P4 / P6
   int il;              // Gram accumulation with the lane's entries interleaved (pipe_gram_acc)
   int zt;              // P2: Z_j rows per lane, transposed Z buffer, vector loads in the Gram loop
-  int oF, oLT, oTau, oG, oU1, oP, oZ, oS, oX2;  // record offsets (doubles)
+  int oF, oLT, oTau, oG, oU1, oP, oZ, oS, oX2, oMs;  // record offsets (doubles)
+  int keepms;          // P2 stores the staged middle slices; P4 / P6 copy them instead of restaging
   int tkeep;           // outputs with t1 <= tkeep keep X2_j = P M_j (all slices) for P6
 };
 
@@ -43,7 +44,7 @@ struct PipeArgs {
 // (work counter); ints at +4: [0] t1, [1] t2, [2] flag (0 live, 1 finished
 // early or dropped), [3] R1, [4] R2; long long at +8: output offset.
 struct PipeRec {
-  double *F, *LT, *tau, *G, *U1, *P, *Z, *sc, *X2;
+  double *F, *LT, *tau, *G, *U1, *P, *Z, *sc, *X2, *Ms;
   int* iv;
   long long* off;
 };
@@ -59,6 +60,7 @@ __device__ __forceinline__ PipeRec pipe_rec(const PipeArgs& a, int slot) {
   q.Z = r + a.oZ;
   q.sc = r + a.oS;
   q.X2 = r + a.oX2;
+  q.Ms = r + a.oMs;
   q.iv = reinterpret_cast<int*>(r + a.oS + 4);
   q.off = reinterpret_cast<long long*>(r + a.oS + 8);
   return q;
@@ -312,6 +314,10 @@ __global__ void __launch_bounds__(NT, 24) pipe_gram1_kernel(PipeArgs a) {
     __syncthreads();
     stage_slices(Ms, p.MSMAX, pt.terms, K, n1, n2, j0, jn);
     __syncthreads();
+    if (a.keepms) {  // the staged slices serve P4 / P6 as plain copies
+      double* mg = r.Ms + (long long)j0 * p.MSMAX;
+      for (int e = threadIdx.x; e < jn * p.MSMAX; e += NT) mg[e] = Ms[e];
+    }
     if (a.zt) {
       pipe_zj_rows(Tb, ldz, Ms, p.MSMAX, pt.terms, pt.rowterm, R3, D3, R1, q3, jn);
       __syncthreads();
@@ -463,7 +469,8 @@ __global__ void __launch_bounds__(NT, 24) pipe_gram2_kernel(PipeArgs a) {
   double* Ms = Tb + JB * D3 * D1;         // JB x MSMAX
   PipeTerms pt = pipe_terms(Ms + JB * p.MSMAX, RM1, RM2);
   int K, R1, R2;
-  setup_terms(p, o, pt.terms, pt.rowterm, pt.colterm, s_meta, K, R1, R2);
+  setup_terms(p, o, pt.terms, pt.rowterm, pt.colterm, s_meta, K, R1, R2, nullptr, 0, nullptr,
+              !a.keepms);
   const int q3 = min(n3, R2);
   pipe_load_r3(R3, D3, r.LT, n3, q3, R2);
   for (int e = threadIdx.x; e < D1 * R1; e += NT) XP[e] = r.P[e];
@@ -473,7 +480,12 @@ __global__ void __launch_bounds__(NT, 24) pipe_gram2_kernel(PipeArgs a) {
   for (int j0 = 0; j0 < n2; j0 += JB) {
     const int jn = min(JB, n2 - j0);
     __syncthreads();
-    stage_slices(Ms, p.MSMAX, pt.terms, K, n1, n2, j0, jn);
+    if (a.keepms) {
+      const double* mg = r.Ms + (long long)j0 * p.MSMAX;
+      for (int e = threadIdx.x; e < jn * p.MSMAX; e += NT) Ms[e] = mg[e];
+    } else {
+      stage_slices(Ms, p.MSMAX, pt.terms, K, n1, n2, j0, jn);
+    }
     __syncthreads();
     left_times_blockdiag_b(X2, t1, t1 * R2, XP, D1, t1, R2, Ms, p.MSMAX, pt.terms, pt.colterm, jn);
     __syncthreads();
@@ -629,12 +641,18 @@ __global__ void __launch_bounds__(NT, 24) pipe_middle_kernel(PipeArgs a) {
     return;
   }
   int K, R1, R2;
-  setup_terms(p, o, pt.terms, pt.rowterm, pt.colterm, s_meta, K, R1, R2);
+  setup_terms(p, o, pt.terms, pt.rowterm, pt.colterm, s_meta, K, R1, R2, nullptr, 0, nullptr,
+              !a.keepms);
   for (int e = threadIdx.x; e < D1 * R1; e += NT) XP[e] = r.P[e];
   for (int j0 = 0; j0 < n2; j0 += JB) {
     const int jn = min(JB, n2 - j0);
     __syncthreads();
-    stage_slices(Ms, p.MSMAX, pt.terms, K, n1, n2, j0, jn);
+    if (a.keepms) {
+      const double* mg = r.Ms + (long long)j0 * p.MSMAX;
+      for (int e = threadIdx.x; e < jn * p.MSMAX; e += NT) Ms[e] = mg[e];
+    } else {
+      stage_slices(Ms, p.MSMAX, pt.terms, K, n1, n2, j0, jn);
+    }
     __syncthreads();
     left_times_blockdiag_b(X2, t1, t1 * R2, XP, D1, t1, R2, Ms, p.MSMAX, pt.terms, pt.colterm, jn);
     __syncthreads();
@@ -684,6 +702,13 @@ static void pipe_layout(PipeArgs& a) {
   }();
   a.tkeep = std::min(tkeep_env, RM1);
   o += even((long long)p.n2 * a.tkeep * RM2);
+  static const int keepms_env = [] {  // TTDVM_PIPE_KEEPMS=0: P4 / P6 restage from the operands (A/B)
+    const char* e = getenv("TTDVM_PIPE_KEEPMS");
+    return e ? atoi(e) : 1;
+  }();
+  a.keepms = keepms_env;
+  a.oMs = (int)o;
+  if (a.keepms) o += even((long long)p.n2 * p.MSMAX);
   a.stride = (o + 15) / 16 * 16;
 }
 
