@@ -309,15 +309,22 @@ __global__ void __launch_bounds__(NT, 24) pipe_gram1_kernel(PipeArgs a) {
   int ei[Q], ej[Q];
   double gh[Q], gl[Q];
   pipe_gram_init<Q>(R1, ei, ej, gh, gl);
+  if (a.keepms) {
+    // every slice of every summand staged ONCE, straight into the record
+    // (one set-up of the Kronecker indices per summand, all lanes busy over
+    // the 44 slices); the batches below and P4 / P6 read plain copies
+    stage_slices(r.Ms, p.MSMAX, pt.terms, K, n1, n2, 0, n2);
+  }
   for (int j0 = 0; j0 < n2; j0 += JB) {
     const int jn = min(JB, n2 - j0);
-    __syncthreads();
-    stage_slices(Ms, p.MSMAX, pt.terms, K, n1, n2, j0, jn);
-    __syncthreads();
-    if (a.keepms) {  // the staged slices serve P4 / P6 as plain copies
-      double* mg = r.Ms + (long long)j0 * p.MSMAX;
-      for (int e = threadIdx.x; e < jn * p.MSMAX; e += NT) mg[e] = Ms[e];
+    __syncthreads();  // (first pass: the record's slices written by this CTA are visible)
+    if (a.keepms) {
+      const double* mg = r.Ms + (long long)j0 * p.MSMAX;
+      for (int e = threadIdx.x; e < jn * p.MSMAX; e += NT) Ms[e] = mg[e];
+    } else {
+      stage_slices(Ms, p.MSMAX, pt.terms, K, n1, n2, j0, jn);
     }
+    __syncthreads();
     if (a.zt) {
       pipe_zj_rows(Tb, ldz, Ms, p.MSMAX, pt.terms, pt.rowterm, R3, D3, R1, q3, jn);
       __syncthreads();
