@@ -713,6 +713,14 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
     // in a per-CTA global scratch slice, persistent CTAs
     l.spill = !use_tsqr &&
               round_gram_smem_bytes(n, n, l.rm1, l.rm2, l.ms, 1, false) > kSmemMax;
+    // TTDVM_SPILL_D=d (experiment): bins with Gram dimension >= d take the
+    // spill plan although they fit shared memory -- their CTAs then need
+    // ~80 KB instead of ~200 KB and can share an SM with the pipeline's
+    static const int spill_d = [] {
+      const char* e = getenv("TTDVM_SPILL_D");
+      return e ? atoi(e) : 0;
+    }();
+    if (spill_d > 0 && !use_tsqr && gram_d(l.rm1, l.rm2) >= spill_d) l.spill = true;
     if (l.spill) l.narrow = false;
     if (!use_tsqr && !l.spill) {
       int k0 = 1, k1 = 1;
@@ -866,7 +874,10 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
         l.pipe_off = pipe_need;
         pipe_need += (size_t)l.pipe_chunk * (size_t)l.pipe_stride;
       }
-      if (pipe_need) c->d_pipe.alloc(pipe_need);
+      // 30 % headroom on growth: the bins' record strides creep up with the
+      // ranks, and regrowing a multi-GB block by a few MB every step costs a
+      // cudaFree + cudaMalloc (tens of ms) each time
+      if (pipe_need > c->d_pipe.n) c->d_pipe.alloc(pipe_need + pipe_need * 3 / 10);
       bool used_aux[3] = {false, false, false};
       if (fork) {
         if (!c->fork_ev) {
