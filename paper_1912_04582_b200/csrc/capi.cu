@@ -382,6 +382,7 @@ struct ttdvm_ctx {
   DevBuf<int> d_bins, d_olist;  // rank bins of the current rounding launch
   DevBuf<double> d_gscratch;     // per-CTA slices of spill-plan rounding launches
   DevBuf<double> d_pipe;         // per-output records of the phase-pipeline launches
+  long long pipe_budget = 0;     // bytes of records per pipelined bin (fixed at the first sizing)
   DevBuf<long long> d_tmp_off;
   DevBuf<double> d_tmp;
   bool profiling = false;
@@ -867,9 +868,21 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
       // concurrently), each a chunk of at most kPipeChunk outputs
       // (at most 65,536 outputs and about 2 GB of records)
       size_t pipe_need = 0;
+      long long pipe_budget = 2LL << 30;  // bytes of records per pipelined bin
+      {
+        bool any = false;
+        for (const Launch& l : plan) any = any || l.pipe;
+        if (any && c->pipe_budget == 0) {  // first sizing: leave memory-tight runs their arenas
+          size_t fr = 0, tot = 0;
+          if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+            pipe_budget = std::min<long long>(pipe_budget, std::max<long long>(256LL << 20, (long long)(fr / 16)));
+          c->pipe_budget = pipe_budget;
+        }
+        if (c->pipe_budget) pipe_budget = c->pipe_budget;
+      }
       for (Launch& l : plan) {
         if (!l.pipe) continue;
-        const long long fit = (2LL << 30) / (8 * std::max<long long>(1, l.pipe_stride));
+        const long long fit = pipe_budget / (8 * std::max<long long>(1, l.pipe_stride));
         l.pipe_chunk = (int)std::min<long long>(std::min(l.count, 65536), std::max<long long>(8192, fit));
         l.pipe_off = pipe_need;
         pipe_need += (size_t)l.pipe_chunk * (size_t)l.pipe_stride;
@@ -877,7 +890,15 @@ void run_round(ttdvm_ctx* c, const TermList& tl, TensorSet* const sets[kMaxSets]
       // 30 % headroom on growth: the bins' record strides creep up with the
       // ranks, and regrowing a multi-GB block by a few MB every step costs a
       // cudaFree + cudaMalloc (tens of ms) each time
-      if (pipe_need > c->d_pipe.n) c->d_pipe.alloc(pipe_need + pipe_need * 3 / 10);
+      if (pipe_need > c->d_pipe.n) {
+        try {
+          c->d_pipe.alloc(pipe_need + pipe_need * 3 / 10);
+        } catch (const Fail& e) {
+          // no room for the records: these bins take the one-kernel path
+          if (e.code != TTDVM_ENOMEM) throw;
+          for (Launch& l : plan) l.pipe = false;
+        }
+      }
       bool used_aux[3] = {false, false, false};
       if (fork) {
         if (!c->fork_ev) {
@@ -2189,8 +2210,26 @@ void download_set(ttdvm_ctx* c, const TensorSet& s, double* cores, int64_t capac
   c->d_tmp_off.alloc(s.count);
   long long maxsz = 1;
   for (int t = 0; t < s.count; ++t) maxsz = std::max<long long>(maxsz, offs[t + 1] - offs[t]);
-  const long long lim = std::max(maxsz, std::min(total, chunk));
-  c->d_tmp.alloc((size_t)lim);
+  long long lim = std::max(maxsz, std::min(total, chunk));
+  // Memory-tight runs (config 5 holds the device within a few GB): when the
+  // staging buffer does not fit, release the rounding scratch (dead between
+  // calls) and then halve the chunk down to the largest tensor.
+  for (;;) {
+    try {
+      c->d_tmp.alloc((size_t)lim);
+      break;
+    } catch (const Fail& e) {
+      if (e.code != TTDVM_ENOMEM) throw;
+      if (c->d_pipe.p || c->d_gscratch.p) {
+        CK(cudaStreamSynchronize(c->st));
+        c->d_pipe.free();
+        c->d_gscratch.free();
+        continue;
+      }
+      if (lim <= maxsz) throw;
+      lim = std::max(maxsz, lim / 2);
+    }
+  }
   int t0 = 0;
   while (t0 < s.count) {
     // chunks are bounded by the requested chunk size, not by the staging
