@@ -531,11 +531,16 @@ def kernel_rooflines(rep, steps, fp64_peak, hbm_peak):
     the measured DFMA peak and the measured HBM bandwidth."""
     kernels = {"moments": ("macro_kernel", "hbm"), "shakhov_build": ("shakhov_raw_kernel", "hbm"),
                "wall_densities": ("wall_kernel", "latency"),
-               "round_fs": ("round_gram_kernel<g32> (f_S)", "fp64"),
-               "round_collision": ("round_gram_kernel<g32> (f_S - f)", "fp64"),
-               "round_flux": ("round_gram_kernel (face fluxes)", "fp64"),
-               "round_residual": ("round_gram_kernel (cell residuals)", "fp64"),
-               "round_update": ("round_gram_kernel (f + dt R)", "fp64")}
+               # bulk rank bins: the six pipe_* phase kernels (round_pipe.cuh); the other
+               # bins: round_gram_kernel at 32 / 128 / 256 / 512 threads
+               "round_fs": ("rounding of f_S (pipe_* phase kernels)", "fp64"),
+               "round_collision": ("rounding of f_S - f (pipe_* phase kernels + round_gram_kernel)", "fp64"),
+               "round_flux": ("rounding of face fluxes (pipe_* phase kernels + round_gram_kernel "
+                              "high-rank bins)", "fp64"),
+               "round_residual": ("rounding of cell residuals (pipe_* phase kernels + "
+                                  "round_gram_kernel high-rank bins)", "fp64"),
+               "round_update": ("rounding of f + dt R (pipe_* phase kernels + round_gram_kernel)",
+                                "fp64")}
     out = {}
     for name, (kern, bound) in kernels.items():
         ms, fl, by, la = rep[name]
