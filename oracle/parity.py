@@ -21,6 +21,18 @@ oracle decision on the mismatching tensor's dependency chain (a cell's new
 state depends on its faces' fluxes, its f_S, J_r and R roundings): if every
 upstream margin is wider than TIE, both sides take the same decisions and
 the ranks must be identical.  No unexplained flips are allowed.
+
+Intermediate stages.  TIE is the window for a decision on IDENTICAL inputs.
+Inside a step the later roundings see inputs that already differ between
+two implementations: two truncated SVDs of the same operand agree only to
+~u ||A|| / gap in the kept subspace (observed 1e-9 relative on face fluxes
+at eps 1e-5), and the residual R_i = J_i + sum_f c_f Phi_f cancels, so its
+rounding sees that difference amplified by kappa = (sum |c_f| ||Phi_f|| +
+||J||) / ||R||: a decision margin up to ~2 sqrt(2) 1e-9 kappa / eps can
+flip legitimately (kappa ~ 30-70 in smooth flow gives ~1 %).  bench.py's
+parity block reports such intermediate flips with their margin and kappa as
+diagnostics; the pass bar is BASELINE.json's, on the state: reconstructions
+within 10 eps, macroparameters within 1e-8, state ranks identical up to TIE.
 """
 from __future__ import annotations
 

@@ -188,6 +188,16 @@ class RefSolver:
         return TtBatch(self.nv, self.nv, self.nv, ranks[:2 * n].reshape(-1, 2), offs,
                        cores[:int(offs[-1])])
 
+    def ranks_of(self, which: int) -> np.ndarray:
+        """(r1, r2) of every tensor of a stage set (layout only)."""
+        cnt = C.c_int32(0)
+        self._check(self.L.ttref_layout(self.h, which, C.byref(cnt), None, None))
+        n = cnt.value
+        ranks = np.zeros(2 * max(n, 1), dtype=np.int32)
+        offs = np.zeros(n + 1, dtype=np.int64)
+        self._check(self.L.ttref_layout(self.h, which, None, _ptr(ranks), _ptr(offs)))
+        return ranks[:2 * n].reshape(-1, 2)
+
     def state(self):
         return self.fetch(self.STATE)
 

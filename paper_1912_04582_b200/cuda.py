@@ -235,6 +235,16 @@ class Context:
                            lambda r, o: self.lib.ttdvm_cuda_stage_layout(self.h, sid, None, r, o),
                            lambda c, cap: self.lib.ttdvm_cuda_stage_download(self.h, sid, c, cap))
 
+    def stage_ranks(self, name: str) -> np.ndarray:
+        """(r1, r2) of every tensor of an intermediate set of the last step (no core download)."""
+        sid = STAGE[name]
+        cnt = C.c_int32()
+        self._check(self.lib.ttdvm_cuda_stage_layout(self.h, sid, C.byref(cnt), None, None))
+        ranks = np.zeros(2 * max(cnt.value, 1), dtype=np.int32)
+        offs = np.zeros(cnt.value + 1, dtype=np.int64)
+        self._check(self.lib.ttdvm_cuda_stage_layout(self.h, sid, None, _ptr(ranks), _ptr(offs)))
+        return ranks[:2 * cnt.value].reshape(-1, 2)
+
     # -- the hot path ----------------------------------------------------------------
     def step(self, dt: float, eps: float, cap: int = 0, nsteps: int = 1):
         """explicit_step, nsteps times, state resident."""
