@@ -330,13 +330,13 @@ def parity_block(p, st_prev, st_new, macros_prev, from_step: int, ncells: int = 
             so = OracleSolver(part.mesh, p.nv, p.bound, p.gas, p.bcs)
             cmx = parity.ChainMargins(so, dict(enumerate(parity.oracle_list(loc))), p.dt, p.eps, p.cap)
             if len(phi_flip):
-                stage["max_phi_flip_margin"] = max(cmx.phi(int(j)) for j in phi_flip[:16])
-            for k in j_flip[:16]:  # the f_S rounding and the (f_S - f) rounding of the cell
+                stage["max_phi_flip_margin"] = max(cmx.phi(int(j)) for j in phi_flip[:4])
+            for k in j_flip[:4]:  # the f_S rounding and the (f_S - f) rounding of the cell
                 m_fs, m_j, _ = cmx.collision(int(k))
                 stage["max_collision_flip_margin"] = max(stage["max_collision_flip_margin"],
                                                          min(m_fs, m_j))
             kappa = 0.0
-            for k in res_flip[:16]:
+            for k in res_flip[:4]:
                 # a residual's inputs (the rounded fluxes) already differ between the two
                 # sides by the roundoff of their own truncations (~u/eps, observed 1e-9);
                 # the residual rounding sees that difference amplified by the
