@@ -284,7 +284,10 @@ __device__ __forceinline__ void pipe_gram_acc_t(double (&gh)[Q], double (&gl)[Q]
 
 // ---- P2 ---------------------------------------------------------------------
 template <int Q>
-__global__ void __launch_bounds__(NT, 24) pipe_gram1_kernel(PipeArgs a) {
+#ifndef TTDVM_PIPE_P2_MINB
+#define TTDVM_PIPE_P2_MINB 24
+#endif
+__global__ void __launch_bounds__(NT, TTDVM_PIPE_P2_MINB) pipe_gram1_kernel(PipeArgs a) {
   extern __shared__ __align__(16) double sm[];
   __shared__ __align__(8) int s_meta[10];
   const int slot = blockIdx.x;
