@@ -134,6 +134,13 @@ __device__ __forceinline__ int floor_pow2(int x) {
 // One-sided (Hestenes) Jacobi on the columns of X (m x c, ld ldx) with
 // tracked squared column norms (one dot product per pair and round; the
 // norms are refreshed at every sweep).
+// TTDVM_JACOBI_UNROLL: unroll factor of the row loops of a pair (1 in the
+// rounding kernels, whose instruction footprint matters; facefactor.cu,
+// latency-bound at 8 warps per SM, batches the loads of 4 rows).
+#ifndef TTDVM_JACOBI_UNROLL
+#define TTDVM_JACOBI_UNROLL 1
+#endif
+constexpr int kJacobiUnroll = TTDVM_JACOBI_UNROLL;
 template <int TPP>
 __device__ int jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
   const int cp = c + (c & 1);
@@ -163,10 +170,15 @@ __device__ int jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
         b += 1;
         const bool live = pp < npairs && a < c && b < c;
         double ga = 0.0;
+#if TTDVM_JACOBI_UNROLL > 1
+        double* __restrict__ x = X + ldx * (live ? a : 0);  // a != b: distinct columns
+        double* __restrict__ y = X + ldx * (live ? b : 0);
+#else
         double* x = X + ldx * (live ? a : 0);
         double* y = X + ldx * (live ? b : 0);
+#endif
         if (live)
-#pragma unroll 1
+#pragma unroll kJacobiUnroll
           for (int i = sub; i < m; i += TPP) ga += x[i] * y[i];
         ga = group_sum<TPP>(ga);
         if (live && ga != 0.0) {
@@ -187,7 +199,7 @@ __device__ int jacobi_t(double* X, int ldx, int m, int c, double* nrm) {
             const double t = (double)tf;
             rotated = rotated || (tf != 0.0f);  // an FP32-underflowed angle is converged
             const double cs = fast_rsqrt(1.0 + t * t), sn = cs * t;
-#pragma unroll 1
+#pragma unroll kJacobiUnroll
             for (int i = sub; i < m; i += TPP) {
               const double xi = x[i], yi = y[i];
               x[i] = cs * xi - sn * yi;
@@ -334,15 +346,16 @@ __device__ __noinline__ int chol_piv_dd(double* Gh, double* Gl, int d, double th
     }
     if (!(bv > thresh)) break;  // uniform: every warp found the same maximum
     __syncthreads();            // everyone has read piv
-    if (threadIdx.x == 0) {
-      const int q = piv[k];
-      piv[k] = piv[bi];
-      piv[bi] = q;
-      for (int r = 0; r < k; ++r) {  // earlier rows of R follow the column swap
+    if (bi != k)  // earlier rows of R follow the column swap (one row per thread)
+      for (int r = threadIdx.x; r < k; r += NT) {
         const double a = R[r + ldr * k];
         R[r + ldr * k] = R[r + ldr * bi];
         R[r + ldr * bi] = a;
       }
+    if (threadIdx.x == 0) {
+      const int q = piv[k];
+      piv[k] = piv[bi];
+      piv[bi] = q;
       const int o = piv[k];
       const double ah = Gh[o + d * o], al = Gl[o + d * o];
       const double s = sqrt(ah);

@@ -1,8 +1,8 @@
-# source-line instruction counts of the LONGEST launch of one pipeline kernel (arg1: kernel regex) in config-4 steps (half scale)
+# source-line instruction counts of the LONGEST launch of one kernel (arg1: kernel regex; arg2/3: launch skip/count; arg4: steps) in config-4 steps (half scale)
 REP=/tmp/pipe_src.ncu-rep
 rm -f $REP
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${1:-pipe_gram1} -s ${2:-12} -c ${3:-12} -o ${REP%.ncu-rep} \
-  python scripts/probe_config4.py --scale 0.5 --steps 3 > gpurun_out/pipe_src_cap.log 2>&1
+  python scripts/probe_config4.py --scale 0.5 --steps ${4:-3} > gpurun_out/pipe_src_cap.log 2>&1
 echo rc=$?
 ncu -i $REP --page raw --csv --metrics gpu__time_duration.sum,launch__grid_size > /tmp/l.csv 2>&1
 B=$(python - <<'PY'
