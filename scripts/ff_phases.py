@@ -27,3 +27,6 @@ tot = cyc[:12].sum()
 print(f"{N} normals {el:.3f}s {el / N * 1e6:.1f} us/normal; {tot / N / 1e6:.2f} Mcycles of CTA residency per normal")
 for nm, c in zip(names, cyc[:12]):
     print("  %-20s %5.1f%%  %8.0f kcyc/normal" % (nm, 100 * c / tot, c / N / 1e3))
+print("  inside the svd phases: pivoted dd Cholesky %.0f kcyc/normal, svd_from_r (Jacobi) %.0f kcyc/normal; "
+      "mean Cholesky rank %.1f over %d factorizations per normal" %
+      (cyc[12] / N / 1e3, cyc[13] / N / 1e3, cyc[14] / max(cyc[15], 1), cyc[15] / N))
