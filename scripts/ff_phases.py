@@ -6,10 +6,14 @@ import numpy as np
 from paper_1912_04582_b200 import cuda
 from paper_1912_04582_b200.cuda import Context
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+LATTICE_ONLY = len(sys.argv) > 2 and sys.argv[2] == "lattice"  # config 4's kind: jittered hex faces only
 rng = np.random.default_rng(0)
 v = rng.normal(size=(N, 3))
 ax = np.eye(3)[rng.integers(0, 3, N // 2)] * rng.choice([-1.0, 1.0], (N // 2, 1))
 v[: N // 2] = ax + 0.1 * rng.normal(size=(N // 2, 3))
+if LATTICE_ONLY:
+    ax = np.eye(3)[rng.integers(0, 3, N)] * rng.choice([-1.0, 1.0], (N, 1))
+    v = ax + 0.05 * rng.normal(size=(N, 3))
 v /= np.linalg.norm(v, axis=1, keepdims=True)
 ctx = Context(0)
 ctx.set_grid(44, 7.0)
