@@ -103,6 +103,97 @@ __device__ __forceinline__ void pipe_load_r3(double* R3, int ld, const double* L
   }
 }
 
+// Householder QR of A (m x c, m <= 64, ld lda) by ONE warp with the lanes over
+// the ROWS (two per lane, in registers for the current reflector): every
+// trailing column costs two FMAs, one warp sum and two FMAs per lane, and
+// four columns are in flight at a time.  qr_grp's column-owner layout leaves
+// a one-warp CTA with two lanes per column and the finished columns' lanes
+// idle (~7.5k warp instructions for 44 x 12 against ~1.7k here).  Same
+// reflector format (larfg, scaled tails below the diagonal, tau) -- the sums
+// are associated differently, as they already are between the 32- and
+// 128-thread builds of qr_grp.
+#ifndef TTDVM_PIPE_QR_ROWS
+#define TTDVM_PIPE_QR_ROWS 1
+#endif
+__device__ __forceinline__ void pipe_qr_rows(double* A, int lda, int m, int c, double* tau) {
+  const int lane = threadIdx.x & 31;
+  const int i0 = lane, i1 = lane + 32;
+  const int kmax = min(m, c);
+  for (int k = 0; k < kmax; ++k) {
+    double* ck = A + lda * k;
+    const bool in0 = i0 > k && i0 < m, in1 = i1 > k && i1 < m;
+    double v0 = in0 ? ck[i0] : 0.0, v1 = in1 ? ck[i1] : 0.0;
+    const double s2 = warp_sum(v0 * v0 + v1 * v1);
+    double beta, t, sc;
+    larfg(ck[k], s2, beta, t, sc);  // every lane: same inputs, same result
+    __syncwarp();
+    if (lane == 0) {
+      tau[k] = t;
+      if (t != 0.0) ck[k] = beta;
+    }
+    if (t == 0.0) continue;
+    v0 *= sc;
+    v1 *= sc;
+    if (in0) ck[i0] = v0;
+    if (in1) ck[i1] = v1;
+    int l = k + 1;
+    for (; l + 3 < c; l += 4) {
+      double* c0 = A + lda * l;
+      double* c1 = c0 + lda;
+      double* c2 = c1 + lda;
+      double* c3 = c2 + lda;
+      const double a00 = in0 ? c0[i0] : 0.0, a01 = in1 ? c0[i1] : 0.0;
+      const double a10 = in0 ? c1[i0] : 0.0, a11 = in1 ? c1[i1] : 0.0;
+      const double a20 = in0 ? c2[i0] : 0.0, a21 = in1 ? c2[i1] : 0.0;
+      const double a30 = in0 ? c3[i0] : 0.0, a31 = in1 ? c3[i1] : 0.0;
+      double w0 = v0 * a00 + v1 * a01, w1 = v0 * a10 + v1 * a11;
+      double w2 = v0 * a20 + v1 * a21, w3 = v0 * a30 + v1 * a31;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        w0 += __shfl_xor_sync(0xffffffffu, w0, o);
+        w1 += __shfl_xor_sync(0xffffffffu, w1, o);
+        w2 += __shfl_xor_sync(0xffffffffu, w2, o);
+        w3 += __shfl_xor_sync(0xffffffffu, w3, o);
+      }
+      w0 = t * (w0 + c0[k]);
+      w1 = t * (w1 + c1[k]);
+      w2 = t * (w2 + c2[k]);
+      w3 = t * (w3 + c3[k]);
+      __syncwarp();  // every lane has read row k
+      if (in0) {
+        c0[i0] = a00 - w0 * v0;
+        c1[i0] = a10 - w1 * v0;
+        c2[i0] = a20 - w2 * v0;
+        c3[i0] = a30 - w3 * v0;
+      }
+      if (in1) {
+        c0[i1] = a01 - w0 * v1;
+        c1[i1] = a11 - w1 * v1;
+        c2[i1] = a21 - w2 * v1;
+        c3[i1] = a31 - w3 * v1;
+      }
+      if (lane == 0) {
+        c0[k] -= w0;
+        c1[k] -= w1;
+        c2[k] -= w2;
+        c3[k] -= w3;
+      }
+    }
+    for (; l < c; ++l) {
+      double* c0 = A + lda * l;
+      const double a00 = in0 ? c0[i0] : 0.0, a01 = in1 ? c0[i1] : 0.0;
+      double w0 = warp_sum(v0 * a00 + v1 * a01);
+      w0 = t * (w0 + c0[k]);
+      __syncwarp();
+      if (in0) c0[i0] = a00 - w0 * v0;
+      if (in1) c0[i1] = a01 - w0 * v1;
+      if (lane == 0) c0[k] -= w0;
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+}
+
 // ---- P1 ---------------------------------------------------------------------
 __global__ void __launch_bounds__(NT, 16) pipe_prep_kernel(PipeArgs a) {
   extern __shared__ __align__(16) double sm[];
@@ -121,7 +212,8 @@ __global__ void __launch_bounds__(NT, 16) pipe_prep_kernel(PipeArgs a) {
   setup_terms(p, o, pt.terms, pt.rowterm, pt.colterm, s_meta, K, R1, R2);
   materialise_outer(F, lastT, pt.terms, K, n1, n2, n3);
   __syncthreads();
-  qr_grp(lastT, n3, n3, R2, tau, sh);
+  if (TTDVM_PIPE_QR_ROWS && n3 <= 64) pipe_qr_rows(lastT, n3, n3, R2, tau);
+  else qr_grp(lastT, n3, n3, R2, tau, sh);
   __syncthreads();
   PipeRec r = pipe_rec(a, slot);
   for (int e = threadIdx.x; e < n1 * R1; e += NT) r.F[e] = F[e];
@@ -590,7 +682,39 @@ __global__ void __launch_bounds__(NT, 12) pipe_factor2_kernel(PipeArgs a) {
   const int kmax = min(n3, R2);
   {  // the warp applies Q3 = H_0 ... H_{kmax-1} to each column of G, lanes over rows
     const int lane = threadIdx.x & 31;
-    for (int s = 0; s < t2; ++s) {
+    int s = 0;
+    for (; TTDVM_PIPE_QR_ROWS && s + 1 < t2; s += 2) {  // two columns in flight (same sums per column)
+      double* g = Xq + n3 * s;
+      double* h = g + n3;
+      for (int k = kmax - 1; k >= 0; --k) {
+        const double t = tau[k];
+        if (t == 0.0) continue;
+        const double* v = lastT + n3 * k;
+        double w = 0.0, x = 0.0;
+        for (int i = k + 1 + lane; i < n3; i += 32) {
+          w += v[i] * g[i];
+          x += v[i] * h[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          w += __shfl_xor_sync(0xffffffffu, w, o);
+          x += __shfl_xor_sync(0xffffffffu, x, o);
+        }
+        w = t * (w + g[k]);
+        x = t * (x + h[k]);
+        __syncwarp();
+        if (lane == 0) {
+          g[k] -= w;
+          h[k] -= x;
+        }
+        for (int i = k + 1 + lane; i < n3; i += 32) {
+          g[i] -= w * v[i];
+          h[i] -= x * v[i];
+        }
+        __syncwarp();
+      }
+    }
+    for (; s < t2; ++s) {
       double* g = Xq + n3 * s;
       for (int k = kmax - 1; k >= 0; --k) {
         const double t = tau[k];
